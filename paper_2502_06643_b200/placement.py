@@ -1,0 +1,79 @@
+"""Host-side expert placements (the input of the GPU path; not on the GPU).
+
+The paper computes the expert->GPU map offline with two ILPs solved by Gurobi
+ and loads it at serving start.  The GPU
+path takes that map as an ``int32 expert_to_rank[E]`` input (BASELINE
+north_star).  This module provides the two maps the benchmark compares:
+
+* ``contiguous(E, G)`` -- Megatron's baseline: "experts 0 and 1 are assigned
+  to GPU 0, experts 2 and 3 to GPU 1, and so on" (§Baseline).
+  E not divisible by G is an error.
+* ``ilp1_exact(load, G)`` -- ILP 1 (Eqs. (1)-(7)) for one layer,
+  solved exactly by enumerating every partition of the E experts into G
+  non-empty clusters (Eq. 7), minimising O1 = sum_c |T_c - T_bar| (Eqs. 1-3,
+  reading G12 drops Eq. 2's spurious sum over t).  Ties are broken by the
+  lexicographically smallest canonical assignment.  Cluster c is
+  placed on GPU c: ILP 2 (Eqs. 8-15) has no layer pairs at L = 1, so its
+  objective is identically 0 and the identity bijection is optimal.
+
+Harness utility: exhaustive enumeration is meant for E <= 12.
+"""
+
+import numpy as np
+
+
+def contiguous(E, G):
+    if G <= 0 or E % G != 0:
+        raise ValueError(f"contiguous placement needs E % G == 0 (E={E}, G={G})")
+    per = E // G
+    return np.array([e // per for e in range(E)], dtype=np.int32)
+
+
+def _restricted_growth_strings(E, G):
+    """All canonical labelings of partitions of range(E) into exactly G blocks
+    (restricted growth strings): a[0] = 0, a[i] <= max(a[:i]) + 1."""
+    a = [0] * E
+
+    def rec(i, m):
+        if E - i < G - (m + 1):      # not enough experts left to open G blocks
+            return
+        if i == E:
+            if m + 1 == G:
+                yield tuple(a)
+            return
+        for c in range(min(m + 2, G)):
+            a[i] = c
+            yield from rec(i + 1, max(m, c))
+
+    if E == 0:
+        return
+    yield from rec(1, 0)
+
+
+def o1_times_G(load, assign, G):
+    """G * O1 for one layer, in exact integers: sum_c |G*T_c - sum_e P_e|."""
+    load = [int(v) for v in load]
+    total = sum(load)
+    T = [0] * G
+    for e, c in enumerate(assign):
+        T[c] += load[e]
+    return sum(abs(G * t - total) for t in T)
+
+
+def ilp1_exact(load, G):
+    """Exact ILP-1 clustering of one layer.  Returns (assign int32 [E], O1)."""
+    E = len(load)
+    if not 1 <= G <= E:
+        raise ValueError("ILP 1 needs 1 <= G <= E (Eq. 7)")
+    best, best_a = None, None
+    for a in _restricted_growth_strings(E, G):
+        v = o1_times_G(load, a, G)
+        if best is None or v < best or (v == best and a < best_a):
+            best, best_a = v, a
+    return np.array(best_a, dtype=np.int32), best / G
+
+
+def balanced(load, G):
+    """Placement used for the 'balanced' benchmark arm: ILP-1 cluster c -> GPU c."""
+    assign, _ = ilp1_exact(load, G)
+    return assign.astype(np.int32)

@@ -1,0 +1,53 @@
+"""Pins for the host placement utility (ILP 1 exact): SPEC's worked
+example, brute force over all labeled surjective assignments,
+E == G, dominance over the contiguous baseline."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_2502_06643_b200 import placement
+
+
+def test_spec_worked_example():
+    a, o1 = placement.ilp1_exact([7, 1, 1, 1], 2)
+    assert a.tolist() == [0, 1, 1, 1] and o1 == 4.0
+
+
+def test_partition_count_is_stirling():
+    # S(8,4) = 1701 canonical partitions
+    assert sum(1 for _ in placement._restricted_growth_strings(8, 4)) == 1701
+
+
+@pytest.mark.parametrize("E,G", [(5, 2), (6, 3), (7, 4), (6, 6)])
+def test_matches_brute_force(E, G):
+    rng = np.random.default_rng(E * 10 + G)
+    for _ in range(5):
+        load = rng.integers(0, 100, size=E)
+        _, o1 = placement.ilp1_exact(load, G)
+        best = None
+        for a in itertools.product(range(G), repeat=E):
+            if len(set(a)) != G:
+                continue                       # Eq. (7): every cluster non-empty
+            T = np.bincount(a, weights=load, minlength=G)
+            v = np.abs(T - load.sum() / G).sum()
+            best = v if best is None else min(best, v)
+        assert o1 == pytest.approx(best, abs=1e-9)
+
+
+def test_dominates_contiguous():
+    rng = np.random.default_rng(0)
+    for _ in range(10):
+        load = rng.integers(0, 5000, size=8)
+        _, o1 = placement.ilp1_exact(load, 4)
+        c = placement.contiguous(8, 4)
+        assert o1 <= placement.o1_times_G(load, c, 4) / 4 + 1e-9
+
+
+def test_skewed_load_isolates_hot_expert():
+    # the SURVEY App. A.1 seed-0 counts at s = 1.6
+    load = [13514, 7477, 4032, 2562, 1882, 1345, 1085, 871]
+    a = placement.balanced(load, 4)
+    assert a.tolist() == [0, 1, 2, 2, 3, 2, 3, 3]
+    assert sum(1 for v in a if v == a[0]) == 1
