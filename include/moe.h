@@ -1,0 +1,213 @@
+/*
+ * moe.h -- C ABI of libmoe, the B200 (sm_100a) expert-parallel MoE-layer hot
+ * path of MoETuner (arXiv 2502.06643).
+ *
+ * Citation key: P:Lnnn = PAPER.md line nnn (§ named), S:Lnnn = SPEC.md line nnn,
+ * Gnn = a reading of the paper listed in DESIGN.md §3.
+ *
+ * The layer (Fig. background-ep(b)):
+ *   moe_route        top-k gating
+ *   moe_route_stats  load P and co-activation R counts
+ *   moe_dispatch     placement-aware permute + all-to-all
+ *   moe_expert_ffn   grouped SwiGLU expert FFN
+ *   moe_combine      all-to-all back + weighted unpermute
+ *
+ * Conventions that hold for every call:
+ *   - Every tensor argument is a DEVICE pointer owned by the caller unless the
+ *     comment says "host".  Layouts are dense row-major, no padding.
+ *   - bf16 tensors are passed as raw 16-bit patterns (moe_bf16).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All device
+ *     work is enqueued on it; calls return before it completes unless stated.
+ *   - Argument validation is synchronous: on MOE_ERR_INVALID_ARG nothing was
+ *     enqueued.  moe_last_error(ctx) holds a message for the last failure.
+ *   - The library never aborts and never prints.
+ *   - A context is bound to one device and is not thread-safe.
+ *
+ * Ranks.  An EP group has G ranks.  G = config.world real processes (one per
+ * GPU, NCCL between them), or G = config.virtual_ranks ranks emulated inside
+ * one process on one GPU (world must then be 1): the kernels, slot, count and
+ * receive layouts are exactly those of G real ranks, and the all-to-all
+ * becomes device-local row copies (SURVEY §4 "virtual ranks").
+ * Token ownership (G7): source rank s owns a contiguous block of
+ * floor(T/G) + [s < T mod G] tokens.  In virtual mode the T passed to a call
+ * covers all G ranks' tokens concatenated in rank order; in real mode T is
+ * this rank's own token count (may differ per rank, may be 0).
+ */
+#ifndef MOE_H
+#define MOE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct moe_ctx* moe_ctx_t;
+typedef uint16_t moe_bf16;     /* raw bf16 bits, binary compatible with __nv_bfloat16 */
+typedef void* moe_stream_t;    /* cudaStream_t */
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARG = 1,   /* bad argument; nothing enqueued */
+  MOE_ERR_CUDA = 2,          /* a CUDA runtime/driver call failed */
+  MOE_ERR_NCCL = 3,          /* an NCCL call failed */
+  MOE_ERR_CAPACITY = 4,      /* size exceeds what the context was created for */
+  MOE_ERR_UNSUPPORTED = 5,   /* shape/mode not implemented (e.g. H % 64 != 0) */
+  MOE_ERR_DEVICE = 6,        /* latched device-side error (bad expert id ...) */
+  MOE_ERR_TIMEOUT = 7
+} moe_status;
+
+typedef enum { MOE_A2A_NCCL = 0, MOE_A2A_P2P = 1 } moe_a2a_mode;
+
+typedef struct {
+  int32_t max_tokens;     /* upper bound on T of any call (per process) */
+  int32_t hidden;         /* H; multiple of 64 */
+  int32_t ffn;            /* F; multiple of 64 */
+  int32_t num_experts;    /* E; 1..256 (route_stats: E <= 128) */
+  int32_t max_k;          /* upper bound on k; 1..E, <= 16 */
+  int32_t world;          /* real EP ranks (processes); 1 => no NCCL */
+  int32_t rank;           /* this process's rank in [0, world) */
+  int32_t device;         /* CUDA device ordinal */
+  int32_t virtual_ranks;  /* >1 => emulate that many EP ranks (world must be 1) */
+  int32_t a2a_mode;       /* moe_a2a_mode; only MOE_A2A_NCCL is implemented */
+} moe_config;
+
+/* Host-side summary of the last dispatch (optional output of moe_dispatch). */
+typedef struct {
+  int32_t world;                 /* G */
+  int32_t num_local_experts;     /* experts hosted by this process (virtual: E) */
+  int64_t recv_rows;             /* routed rows this process computes */
+  int32_t send_counts[64];       /* rows this rank sends to rank g (real mode) */
+  int32_t recv_counts[64];       /* rows rank g receives (all ranks) */
+} moe_dispatch_info;
+
+/* ---- lifecycle ------------------------------------------------------------ */
+
+/* Create an NCCL unique id (rank 0 only); the caller broadcasts the 128 bytes
+ * (e.g. with torch.distributed).  out: host, 128 bytes. */
+moe_status moe_get_unique_id(uint8_t out[128]);
+
+/* Create a context (collective over the EP group when world > 1).  Allocates
+ * every workspace for the worst case of dropless routing (G6): per process
+ * max_tokens * min(k, E_local) routed rows plus 128-row padding per expert.
+ * uid: host, 128 bytes from moe_get_unique_id, or NULL when world == 1. */
+moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out);
+moe_status moe_ctx_destroy(moe_ctx_t ctx);               /* collective when world > 1 */
+moe_status moe_ctx_sync(moe_ctx_t ctx);                   /* sync the last stream; surfaces MOE_ERR_DEVICE */
+const char* moe_status_str(moe_status s);
+const char* moe_last_error(moe_ctx_t ctx);                /* "" if none; ctx may be NULL */
+int32_t moe_abi_version(void);                            /* MOE_ABI_VERSION */
+#define MOE_ABI_VERSION 1
+
+/* ---- a1: gating (G1, G2, G3) -------------------------------------
+ * For each token t: idx[t][0..k-1] = the k largest logits[t][.] in descending
+ * order, ties to the lower expert id, -0.0 == +0.0; w[t][j] = softmax over the
+ * k selected logits = exp(l_j - l_0) / sum_j' exp(l_j' - l_0) (fp32).
+ * logits: float [T][E]; idx: int32 [T][k]; w: float [T][k].  Rank-local. */
+moe_status moe_route(moe_ctx_t ctx, const float* logits, int32_t T, int32_t E, int32_t k,
+                     int32_t* idx, float* w, moe_stream_t stream);
+
+/* ---- a2: routing statistics (P:L581 P_{e,l}; P:L654 R_{e1,e2,l}; G10) ----------
+ * load[e]        += #{(t,j)      : idx_l[t][j] == e}
+ * coact[e1][e2]  += #{(t,j1,j2)  : idx_l[t][j1] == e1 && idx_l1[t][j2] == e2}
+ * idx_l, idx_l1: int32 [T][k], the same token rows at layers l and l+1
+ * (idx_l1 may be NULL: then coact is not touched).  load: int64 [E],
+ * coact: int64 [E][E] e1-major; both ACCUMULATE (caller zeroes them).
+ * Out-of-range ids latch MOE_ERR_DEVICE.  Rank-local; see moe_stats_allreduce. */
+moe_status moe_route_stats(moe_ctx_t ctx, const int32_t* idx_l, const int32_t* idx_l1,
+                           int32_t T, int32_t E, int32_t k, int64_t* load, int64_t* coact,
+                           moe_stream_t stream);
+
+/* Sum load [E] and coact [E][E] (int64, in place) over the EP group (NCCL
+ * all-reduce).  No-op when world == 1.  coact may be NULL. */
+moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E,
+                               moe_stream_t stream);
+
+/* ---- a3-a5: dispatch (G7, G8, G9, G13, G14) ---
+ * x: bf16 [T][H] (this process's tokens); idx: int32 [T][k] from moe_route.
+ * expert_to_rank: HOST int32 [E], values in [0, G) (the placement input; a rank
+ * may host 0 experts).  Builds the stable send order (key P[e], e, t), the
+ * expert-major receive layout (e ascending on g, then source s, then t; each
+ * expert segment padded to 128 rows) and moves every routed row to the rank
+ * hosting its expert.  Collective when world > 1 (NCCL mode synchronises the
+ * stream once to read the G x E count matrix).  The plan stays in the context
+ * until the next moe_dispatch.  info: host, optional; if non-NULL the call
+ * synchronises `stream` and fills it. */
+moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
+                        const int32_t* expert_to_rank, moe_dispatch_info* info,
+                        moe_stream_t stream);
+
+/* ---- a6: grouped SwiGLU expert FFN (G5) ---------------------------------
+ * For every hosted expert e and its received rows X_e:
+ *   h = bf16( silu(X_e W1_e^T) * (X_e W3_e^T) ),  Y_e = bf16( h W2_e^T )
+ * with fp32 accumulation on tcgen05 tensor cores.  w13: bf16 packed
+ * [n_w][2F][H] (see moe_pack_w13), w2: bf16 [n_w][H][F]; n_w experts in
+ * ascending global id: the hosted experts (real mode) or all E (virtual). */
+moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2,
+                          moe_stream_t stream);
+
+/* ---- a7-a8: combine (G4) -------------------------------------------------
+ * Returns every expert output row to its source rank and writes
+ * out[t] = bf16( sum_{j ascending} w[t][j] * Y[item (t,j)] ) in fp32.
+ * w: float [T][k] (from moe_route); out: bf16 [T][H].  Uses the plan of the
+ * last moe_dispatch (same T, k).  Collective when world > 1. */
+moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_t stream);
+
+/* ---- helpers ---------------------------------------------------------------------- */
+
+/* Pack per-expert W1, W3 ([n][F][H] each) into w13 [n][2F][H]: for every
+ * 128-row block b of F (64 if F % 128 != 0), rows [2b*B, 2b*B+B) = W1 block b and
+ * rows [2b*B+B, 2b*B+2B) = W3 block b, B = block size, so one GEMM N-tile holds
+ * matching gate and up columns.  Device pointers, async on `stream`. */
+moe_status moe_pack_w13(const moe_bf16* w1, const moe_bf16* w3, int32_t n, int32_t F, int32_t H,
+                        moe_bf16* w13, moe_stream_t stream);
+
+/* Megatron's contiguous placement: out[e] = e / (E/G).  out: host
+ * int32 [E].  E % G != 0 => MOE_ERR_INVALID_ARG. */
+moe_status moe_placement_contiguous(int32_t E, int32_t G, int32_t* out);
+
+/* Host-side dispatch layout (the arithmetic NCCL mode uses to post its
+ * send/recv segments; exported for CPU tests).  Inputs host: P [E], cnt [G][E].
+ * Outputs host (any may be NULL):
+ *   seg_start [E]  padded start row of expert e's segment on rank P[e]
+ *   recv_base [G][E] receive row of the first item of (source s, expert e)
+ *   recv_rows [G]  unpadded routed rows received by rank g
+ *   send_base [G][E] position of the first item of (s, e) in s's send order */
+moe_status moe_layout_host(int32_t E, int32_t G, const int32_t* P, const int32_t* cnt,
+                           int32_t* seg_start, int32_t* recv_base, int32_t* recv_rows,
+                           int32_t* send_base);
+
+/* ---- debug / test views (synchronise the context's last stream) ------------------- */
+
+/* Copies the plan of the last moe_dispatch to host arrays sized for the T and k
+ * of that call (any pointer may be NULL):
+ *   dest_rank [T][k]  rank hosting item (t, j)'s expert
+ *   recv_pos  [T][k]  unpadded position of the item in that rank's receive order
+ *   send_slot [T][k]  position of the item in its source's send order (C3 slot)
+ *   cnt       [G][E]  count matrix of all ranks. */
+moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos,
+                          int32_t* send_slot, int32_t* cnt);
+
+/* Expert FFN replaced by the identity (Y = received rows), for bit-exact
+ * dispatch/combine tests (out must equal x). */
+moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream);
+
+/* Copies the received rows of the last dispatch, in unpadded receive order of
+ * this process (virtual: rank 0's rows first, ...), to host bf16 [rows][H]. */
+moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out);
+
+/* Number of kernels this context has launched since creation (for the bench's
+ * gpu_launches count). */
+int64_t moe_kernel_launches(moe_ctx_t ctx);
+
+/* Per-kernel timing of moe_expert_ffn: when enabled, CUDA events are recorded
+ * on the call's stream around the K5 (gate/up + SwiGLU) and K6 (down) GEMM
+ * launches.  moe_ffn_timing_read synchronises on those events and writes the
+ * last call's durations in milliseconds: ms[0] = K5, ms[1] = K6 (host). */
+moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t enable);
+moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_H */

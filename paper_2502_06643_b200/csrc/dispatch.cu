@@ -1,0 +1,424 @@
+// dispatch.cu -- K2 (placement-aware histogram + stable scan), K3 (16-byte
+// vectorised gather/permute into the receive / send buffers) and K8 (fused
+// weighted unpermute / combine).
+//
+// Paper: tokens are "routed to remote GPUs using all-to-all communication based
+// on their assigned experts", with the all-to-all before and after
+// the expert FFN and an arbitrary expert->GPU map.
+// Readings: G7 token blocks, G8 ascending expert order per GPU,
+// G9 send order (P[e], e, t) / receive order (e, s, t), G13 empty ranks.
+//
+// Positions are never taken from atomics: every item's row is
+//   base_row[s][e] + tile_base[tile][e] + (stable rank inside the tile),
+// so the permutation is deterministic and bit-exact with the oracle (C3).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+
+__host__ __device__ __forceinline__ void source_block(int T, int V, int s, int& t0, int& t1) {
+  const int base = T / V, rem = T % V;
+  t0 = s * base + (s < rem ? s : rem);
+  t1 = t0 + base + (s < rem ? 1 : 0);
+}
+
+int plan_tiles(int T, int V) {
+  int n = 0;
+  for (int s = 0; s < V; ++s) {
+    int t0, t1;
+    source_block(T, V, s, t0, t1);
+    n += (t1 - t0 + kTileTokens - 1) / kTileTokens;
+  }
+  return n;
+}
+
+// tile -> (source, first token, end token, first tile of the source)
+__device__ __forceinline__ void tile_info(const PlanArgs& a, int tile, int& s, int& t0, int& t1, int& tile0) {
+  int first = 0;
+  for (s = 0; s < a.V; ++s) {
+    int b0, b1;
+    source_block(a.T, a.V, s, b0, b1);
+    const int nt = (b1 - b0 + kTileTokens - 1) / kTileTokens;
+    if (tile < first + nt) {
+      tile0 = first;
+      t0 = b0 + (tile - first) * kTileTokens;
+      t1 = min(t0 + kTileTokens, b1);
+      return;
+    }
+    first += nt;
+  }
+  s = -1; t0 = t1 = 0; tile0 = first;
+}
+
+// ----------------------------------------------------------------- K2a: per-tile histogram
+__global__ void __launch_bounds__(128) k_count(PlanArgs a, const int32_t* __restrict__ idx, PlanBuffers b) {
+  __shared__ int hist[kMaxExperts];
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  int s, t0, t1, tile0;
+  tile_info(a, blockIdx.x, s, t0, t1, tile0);
+  const int lane = threadIdx.x & 31;
+  const int n = (t1 - t0) * a.k;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    int e = -1;
+    if (i < n) {
+      e = idx[(long long)t0 * a.k + i];
+      if (e < 0 || e >= a.E) {
+        atomicOr(b.err, kErrBadExpert);
+        e = -1;
+      }
+    }
+    unsigned m = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && lane == __ffs(m) - 1) atomicAdd(&hist[e], __popc(m));
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.E; e += blockDim.x) b.tile_hist[(long long)blockIdx.x * a.E + e] = hist[e];
+}
+
+// ----------------------------------------------------------------- K2b: scan over tiles
+// One CTA per local source.  Thread (e, c) sums chunk c of the source's tiles
+// for expert e; chunk partials are scanned per expert; then each thread writes
+// the exclusive prefix of its tiles.  Also emits cnt_local[s][e].
+__global__ void __launch_bounds__(1024) k_scan(PlanArgs a, PlanBuffers b) {
+  __shared__ int part[1024];
+  const int s = blockIdx.x;
+  int tile0 = 0;
+  for (int q = 0; q < s; ++q) {
+    int b0, b1;
+    source_block(a.T, a.V, q, b0, b1);
+    tile0 += (b1 - b0 + kTileTokens - 1) / kTileTokens;
+  }
+  int b0, b1;
+  source_block(a.T, a.V, s, b0, b1);
+  const int nt = (b1 - b0 + kTileTokens - 1) / kTileTokens;
+  const int C = blockDim.x / a.E;  // chunks per expert
+  const int e = threadIdx.x % a.E, c = threadIdx.x / a.E;
+  const bool active = c < C;
+  const int per = (nt + C - 1) / C;
+  const int c0 = min(nt, c * per), c1 = min(nt, c0 + per);
+  int sum = 0;
+  if (active)
+    for (int t = c0; t < c1; ++t) sum += b.tile_hist[(long long)(tile0 + t) * a.E + e];
+  if (active) part[c * a.E + e] = sum;
+  __syncthreads();
+  if (threadIdx.x < a.E) {
+    int run = 0;
+    for (int q = 0; q < C; ++q) {
+      int v = part[q * a.E + threadIdx.x];
+      part[q * a.E + threadIdx.x] = run;
+      run += v;
+    }
+    b.cnt_local[s * a.E + threadIdx.x] = run;
+  }
+  __syncthreads();
+  if (active) {
+    int run = part[c * a.E + e];
+    for (int t = c0; t < c1; ++t) {
+      const long long o = (long long)(tile0 + t) * a.E + e;
+      const int v = b.tile_hist[o];
+      b.tile_base[o] = run;
+      run += v;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K2c: layout (1 CTA)
+// hosted(e) = virtual mode || P[e] == me.  Hosted experts are ordered by key
+// (P[e], e); each segment is padded to kSegAlign rows.  Writes base_row[s][e]
+// (receive row for hosted e, compact send-buffer row for remote e), the GEMM
+// segment table and totals.
+__global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers b, long long cap_rows) {
+  __shared__ int rows_s[kMaxExperts], pad_s[kMaxExperts], key_s[kMaxExperts], hosted_s[kMaxExperts];
+  const int e = threadIdx.x;
+  const int E = a.E;
+  if (e < E) {
+    const int p = b.P[e];
+    int r = 0;
+    for (int s = 0; s < a.G; ++s) r += b.cnt_all[s * E + e];
+    const int hosted = a.virt || p == a.me;
+    rows_s[e] = r;
+    pad_s[e] = hosted ? (r + kSegAlign - 1) / kSegAlign * kSegAlign : 0;
+    key_s[e] = p * E + e;
+    hosted_s[e] = hosted;
+  }
+  __syncthreads();
+  int* nseg = b.seg_meta;
+  int* seg_row0 = b.seg_meta + 1;
+  int* seg_rows = b.seg_meta + 1 + E;
+  int* seg_w = b.seg_meta + 1 + 2 * E;
+  int* totals = b.seg_meta + 1 + 3 * E;  // [0] padded rows, [1] unpadded rows
+  if (e < E) {
+    const int my_key = key_s[e];
+    long long start = 0;
+    int pos = 0, send_base = 0;
+    for (int q = 0; q < E; ++q) {
+      if (key_s[q] < my_key) {
+        if (hosted_s[q]) {
+          start += pad_s[q];
+          ++pos;
+        } else if (!a.virt) {
+          send_base += b.cnt_all[a.me * E + q];
+        }
+      }
+    }
+    if (hosted_s[e]) {
+      seg_row0[pos] = (int)start;
+      seg_rows[pos] = rows_s[e];
+      seg_w[pos] = a.virt ? e : pos;
+      if (start + pad_s[e] > cap_rows) atomicOr(b.err, kErrCapacity);
+    }
+    for (int s = 0; s < a.V; ++s) {
+      const int gs = a.virt ? s : a.me;  // global source id of local source s
+      int base;
+      if (hosted_s[e]) {
+        long long acc = start;
+        for (int q = 0; q < gs; ++q) acc += b.cnt_all[q * E + e];
+        base = (int)acc;
+      } else {
+        base = send_base;
+      }
+      b.base_row[s * E + e] = base;
+    }
+  }
+  if (e == 0) {
+    int n = 0, tp = 0, tu = 0;
+    for (int q = 0; q < E; ++q)
+      if (hosted_s[q]) {
+        ++n;
+        tp += pad_s[q];
+        tu += rows_s[q];
+      }
+    *nseg = n;
+    totals[0] = tp;
+    totals[1] = tu;
+  }
+}
+
+// ----------------------------------------------------------------- K2d + K3: ranks + row copies
+// Per tile: stable in-tile rank of every item among items with the same expert
+// (warp __match_any_sync + per-warp counts), row = base_row + tile_base + rank;
+// then every token row of x is read once (16-byte vectors) and stored k times.
+constexpr int kScatterThreads = 256;
+constexpr int kMaxTileItems = kTileTokens * kMaxK;
+
+struct TileItems {
+  int row[kMaxTileItems];
+  unsigned char remote[kMaxTileItems];
+};
+
+__device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __restrict__ idx, const PlanBuffers& b,
+                                           int tile, int s, int t0, int t1, TileItems& it, int* run, int* wcnt) {
+  const int E = a.E;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) run[e] = 0;
+  const int n = (t1 - t0) * a.k;
+  for (int base = 0; base < n; base += blockDim.x) {
+    for (int q = threadIdx.x; q < nwarps * E; q += blockDim.x) wcnt[q] = 0;
+    __syncthreads();
+    const int i = base + threadIdx.x;
+    int e = -1;
+    if (i < n) {
+      e = idx[(long long)t0 * a.k + i];
+      if (e < 0 || e >= E) e = -1;  // latched by k_count
+    }
+    const unsigned m = __match_any_sync(0xffffffffu, e);
+    const int wrank = __popc(m & ((1u << lane) - 1));
+    if (e >= 0 && wrank == 0) wcnt[warp * E + e] = __popc(m);
+    __syncthreads();
+    if (i < n) {
+      if (e >= 0) {
+        int r = run[e] + wrank;
+        for (int w = 0; w < warp; ++w) r += wcnt[w * E + e];
+        const int p = b.P[e];
+        const int remote = !(a.virt || p == a.me);
+        const int row = b.base_row[s * E + e] + b.tile_base[(long long)tile * E + e] + r;
+        it.row[i] = row;
+        it.remote[i] = (unsigned char)remote;
+        // encoding: row >= 0 local (receive buffer), -(row + 2) remote (send/return buffer), -1 invalid
+        b.row_of_item[(long long)t0 * a.k + i] = remote ? -(row + 2) : row;
+      } else {
+        it.row[i] = -1;
+        it.remote[i] = 0;
+        b.row_of_item[(long long)t0 * a.k + i] = -1;
+      }
+    }
+    __syncthreads();
+    for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
+      int add = 0;
+      for (int w = 0; w < nwarps; ++w) add += wcnt[w * E + e2];
+      run[e2] += add;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const uint4* __restrict__ x,
+                                                             const int32_t* __restrict__ idx, PlanBuffers b,
+                                                             uint4* __restrict__ recv, uint4* __restrict__ sendbuf) {
+  __shared__ TileItems it;
+  __shared__ int run[kMaxExperts];
+  __shared__ int wcnt[(kScatterThreads / 32) * kMaxExperts];
+  int s, t0, t1, tile0;
+  tile_info(a, blockIdx.x, s, t0, t1, tile0);
+  tile_ranks(a, idx, b, blockIdx.x, s, t0, t1, it, run, wcnt);
+  // copy: (token, 16-byte chunk) pairs, consecutive threads -> consecutive chunks
+  const int cpr = a.H / 8;
+  const int k = a.k;
+  const long long total = (long long)(t1 - t0) * cpr;
+  constexpr int U = 4;
+  for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long p = p0 + (long long)u * blockDim.x;
+      if (p < total) {
+        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        v[u] = __ldg(x + (long long)(t0 + tok) * cpr + c);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long p = p0 + (long long)u * blockDim.x;
+      if (p < total) {
+        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        for (int j = 0; j < k; ++j) {
+          const int i = tok * k + j;
+          const int row = it.row[i];
+          if (row >= 0) {
+            uint4* dst = it.remote[i] ? sendbuf : recv;
+            dst[(long long)row * cpr + c] = v[u];
+          }
+        }
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K8: weighted unpermute
+// out[t] = bf16( sum_{j ascending} w[t][j] * Y[item (t,j)] ), fp32 FMA (reading G4).
+__global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const float* __restrict__ w, PlanBuffers b,
+                                                             const uint4* __restrict__ ybuf,
+                                                             const uint4* __restrict__ retbuf,
+                                                             uint4* __restrict__ out) {
+  __shared__ int row_s[kMaxTileItems];
+  __shared__ float w_s[kMaxTileItems];
+  __shared__ unsigned char remote_s[kMaxTileItems];
+  int s, t0, t1, tile0;
+  tile_info(a, blockIdx.x, s, t0, t1, tile0);
+  const int k = a.k;
+  const int n = (t1 - t0) * k;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const long long gi = (long long)t0 * k + i;
+    const int v = b.row_of_item[gi];
+    row_s[i] = v >= 0 ? v : (v == -1 ? -1 : -(v + 2));
+    w_s[i] = w[gi];
+    remote_s[i] = (unsigned char)(v < -1);
+  }
+  __syncthreads();
+  const int cpr = a.H / 8;
+  const long long total = (long long)(t1 - t0) * cpr;
+  constexpr int U = 2;
+  for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
+    float acc[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long p = p0 + (long long)u * blockDim.x;
+        v[u] = make_uint4(0, 0, 0, 0);
+        if (p < total) {
+          const int tok = (int)(p / cpr), c = (int)(p % cpr);
+          const int i = tok * k + j;
+          const int row = row_s[i];
+          if (row >= 0) v[u] = __ldg((remote_s[i] ? retbuf : ybuf) + (long long)row * cpr + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long p = p0 + (long long)u * blockDim.x;
+        if (p < total) {
+          const int tok = (int)(p / cpr);
+          const int i = tok * k + j;
+          const float wj = row_s[i] >= 0 ? w_s[i] : 0.f;
+          acc[u][0] = fmaf(wj, bf16_lo(v[u].x), acc[u][0]);
+          acc[u][1] = fmaf(wj, bf16_hi(v[u].x), acc[u][1]);
+          acc[u][2] = fmaf(wj, bf16_lo(v[u].y), acc[u][2]);
+          acc[u][3] = fmaf(wj, bf16_hi(v[u].y), acc[u][3]);
+          acc[u][4] = fmaf(wj, bf16_lo(v[u].z), acc[u][4]);
+          acc[u][5] = fmaf(wj, bf16_hi(v[u].z), acc[u][5]);
+          acc[u][6] = fmaf(wj, bf16_lo(v[u].w), acc[u][6]);
+          acc[u][7] = fmaf(wj, bf16_hi(v[u].w), acc[u][7]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long p = p0 + (long long)u * blockDim.x;
+      if (p < total) {
+        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        uint4 o;
+        o.x = pack_bf16x2(acc[u][0], acc[u][1]);
+        o.y = pack_bf16x2(acc[u][2], acc[u][3]);
+        o.z = pack_bf16x2(acc[u][4], acc[u][5]);
+        o.w = pack_bf16x2(acc[u][6], acc[u][7]);
+        out[(long long)(t0 + tok) * cpr + c] = o;
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------------- weight packing
+int pack_block(int F) { return (F % 128 == 0) ? 128 : 64; }
+
+__global__ void k_pack_w13(const uint4* __restrict__ w1, const uint4* __restrict__ w3, int n, int F, int H, int B,
+                           uint4* __restrict__ w13) {
+  const int cpr = H / 8;
+  const long long total = (long long)n * 2 * F * cpr;
+  for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < total;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(p % cpr);
+    const long long r2 = p / cpr;            // row in [n*2F]
+    const int ex = (int)(r2 / (2 * F));
+    const int r = (int)(r2 % (2 * F));
+    const int blk = r / (2 * B), within = r % (2 * B);
+    const uint4* src = within < B ? w1 : w3;
+    const int srow = blk * B + (within < B ? within : within - B);
+    w13[p] = src[((long long)ex * F + srow) * cpr + c];
+  }
+}
+
+// ----------------------------------------------------------------- launchers
+void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s) {
+  if (a.n_tiles > 0) k_count<<<a.n_tiles, 128, 0, s>>>(a, idx, b);
+}
+void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s) {
+  k_scan<<<a.V, 1024, 0, s>>>(a, b);
+}
+void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s) {
+  k_layout<<<1, kMaxExperts, 0, s>>>(a, b, (long long)cap_rows);
+}
+void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, uint16_t* recv,
+                    uint16_t* sendbuf, cudaStream_t s) {
+  if (a.n_tiles > 0)
+    k_scatter<<<a.n_tiles, kScatterThreads, 0, s>>>(a, (const uint4*)x, idx, b, (uint4*)recv, (uint4*)sendbuf);
+}
+void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, const uint16_t* ybuf,
+                    const uint16_t* retbuf, uint16_t* out, cudaStream_t s) {
+  if (a.n_tiles > 0)
+    k_combine<<<a.n_tiles, kScatterThreads, 0, s>>>(a, w, b, (const uint4*)ybuf, (const uint4*)retbuf, (uint4*)out);
+}
+void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13, cudaStream_t s) {
+  const long long total = (long long)n * 2 * F * (H / 8);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  k_pack_w13<<<blocks, 256, 0, s>>>((const uint4*)w1, (const uint4*)w3, n, F, H, pack_block(F), (uint4*)w13);
+}
+
+}  // namespace moe

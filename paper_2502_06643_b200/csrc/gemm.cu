@@ -1,0 +1,318 @@
+// gemm.cu -- K5/K6: persistent grouped bf16 GEMM on tcgen05 tensor cores.
+//
+// Computes, for every hosted expert segment i (rows [row0_i, row0_i + rows_i)
+// of the expert-major receive layout, padded to 128 rows):
+//   SWIGLU=true  (K5): acc = A_i W13_i^T (N = 2F, interleaved gate/up blocks of
+//                      BN/2 columns, see moe_pack_w13); D = bf16(silu(g) * u)
+//   SWIGLU=false (K6): D = bf16(A_i W2_i^T)
+// i.e. the Mixtral SwiGLU expert FFN (reading G5) that the paper runs between
+// the two all-to-alls.  fp32 accumulation in TMEM, fixed K order, no
+// split-K: results are bit-identical for a row regardless of placement or G.
+//
+// Structure (one CTA per SM, persistent, static round-robin tile schedule):
+//   warp 0      TMA producer: A tile [128 x 64] + B tile [BN x 64] per stage,
+//               128-byte swizzle, mbarrier complete_tx
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N=BN, K=16 per instruction), tcgen05.commit -> barriers
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (TMEM lane = tile row) -> SwiGLU /
+//               convert -> 16-byte global stores; double-buffered accumulators
+// Tile order: segment, then N tile, then M tile fastest, so the CTAs running
+// concurrently share the same weight tiles (B) and walk the segment's rows (A),
+// which stay resident in the 126 MB L2 across N tiles.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
+constexpr int kGemmThreads = 192;
+constexpr int kSmemBudget = 200 * 1024;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (kSmemBudget / STAGE_BYTES) > 8 ? 8 : (kSmemBudget / STAGE_BYTES);
+  static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                   : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*seg table*/ + 256 /*barriers*/;
+};
+
+struct SegSmem {
+  int nseg;
+  int row0[kMaxExperts];
+  int wrow[kMaxExperts];   // weight index
+  int mtiles[kMaxExperts];
+  int tile0[kMaxExperts + 1];
+};
+
+__device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile, int& arow, int& brow_blk,
+                                            int& ntile) {
+  int i = 0;
+  // segments are few (<= E); linear scan from the last hit would also do
+  while (i + 1 < sg.nseg && tile >= sg.tile0[i + 1]) ++i;
+  const int local = tile - sg.tile0[i];
+  const int mt = sg.mtiles[i];
+  ntile = local / mt;
+  const int mtile = local % mt;
+  arow = sg.row0[i] + mtile * BM;
+  brow_blk = sg.wrow[i];
+  (void)ntn;
+}
+
+template <int BN, bool SWIGLU>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + C::STAGES * C::A_BYTES;
+  SegSmem& sg = *reinterpret_cast<SegSmem*>(smem + C::STAGES * C::STAGE_BYTES);
+  static_assert(sizeof(SegSmem) <= 8192, "segment table");
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 8192);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::STAGES;
+  uint64_t* tfull = bars + 2 * C::STAGES;
+  uint64_t* tempty = bars + 2 * C::STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int ntn = N / BN;
+  const int nkb = K / BK;
+
+  // ---- segment table -> smem (tile prefix over segments)
+  if (threadIdx.x == 0) {
+    const int nseg = seg_meta[0];
+    sg.nseg = nseg;
+    int acc = 0;
+    for (int i = 0; i < nseg; ++i) {
+      const int rows = seg_meta[1 + E + i];
+      const int mt = (rows + BM - 1) / BM;
+      sg.row0[i] = seg_meta[1 + i];
+      sg.wrow[i] = seg_meta[1 + 2 * E + i] * N;
+      sg.mtiles[i] = mt;
+      sg.tile0[i] = acc;
+      acc += mt * ntn;
+    }
+    sg.tile0[nseg] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total_tiles = sg.tile0[sg.nseg];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int arow, bblk, nt;
+        decode_tile(sg, ntn, tile, arow, bblk, nt);
+        const int brow = bblk + nt * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(&tmA, &full[stage], smA + stage * C::A_BYTES, kb * BK, arow);
+          tma_load_2d(&tmB, &full[stage], smB + stage * C::B_BYTES, kb * BK, brow);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer (single thread)
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smA + stage * C::A_BYTES);
+          const uint32_t b_addr = smem_u32(smB + stage * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            umma_bf16(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                      (kb | kk) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ================= epilogue warps 2..5 (TMEM lane quarter = warp % 4)
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int arow, bblk, nt;
+      decode_tile(sg, ntn, tile, arow, bblk, nt);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const long long grow = arow + q * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      if constexpr (SWIGLU) {
+        uint16_t* drow = D + grow * ldd + (long long)nt * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(taddr + c, g);
+          tmem_ld32(taddr + BN / 2 + c, u);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+            const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+            const float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+            const float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+            packed[i] = pack_bf16x2(h0, h1);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(drow + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+        }
+      } else {
+        uint16_t* drow = D + grow * ldd + (long long)nt * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          uint4* dst = reinterpret_cast<uint4*>(drow + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+int gemm_block_n(int N, bool swiglu) {
+  if (swiglu) return (N % 256 == 0 && (N / 2) % 128 == 0) ? 256 : 128;
+  if (N % 256 == 0) return 256;
+  if (N % 128 == 0) return 128;
+  return 64;
+}
+
+template <int BN, bool SWIGLU>
+static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
+                               int N, int K, int num_sms, cudaStream_t s) {
+  using C = GemmCfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_grouped_gemm<BN, SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(tmA);
+  const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(tmB);
+  k_grouped_gemm<BN, SWIGLU><<<num_sms, kGemmThreads, C::SMEM, s>>>(a, b, D, ldd, seg_meta, E, N, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
+                                int E, int N, int K, bool swiglu, int num_sms, cudaStream_t s) {
+  const int bn = gemm_block_n(N, swiglu);
+  if (swiglu) {
+    if (bn == 256) return launch_impl<256, true>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+    return launch_impl<128, true>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+  }
+  if (bn == 256) return launch_impl<256, false>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+  if (bn == 128) return launch_impl<128, false>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+  return launch_impl<64, false>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace moe

@@ -1,0 +1,742 @@
+// moe_api.cu -- the C ABI of libmoe (include/moe.h): context, validation,
+// workspace ownership, NCCL orchestration of the all-to-all, launches.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/moe.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace moe;
+
+struct moe_ctx {
+  moe_config cfg{};
+  int G = 1, V = 1, me = 0, virt = 0;
+  int num_sms = 148;
+  int E = 0, H = 0, F = 0;
+  cudaStream_t last_stream = nullptr;
+  ncclComm_t comm = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // placement
+  int32_t* P_dev = nullptr;
+  int32_t* P_pinned = nullptr;
+  std::vector<int32_t> P_host;
+  bool P_valid = false;
+
+  // plan workspaces
+  int max_tiles = 0;
+  int32_t* tile_hist = nullptr;
+  int32_t* tile_base = nullptr;
+  int32_t* cnt_local = nullptr;
+  int32_t* cnt_all = nullptr;
+  int32_t* base_row = nullptr;
+  int32_t* seg_meta = nullptr;
+  int32_t* row_of_item = nullptr;
+  int* err_dev = nullptr;
+  int32_t* cnt_pinned = nullptr;  // host copy of cnt_all (NCCL mode / debug)
+
+  // payload buffers
+  int64_t cap_rows = 0;      // receive-layout rows (padded)
+  int64_t send_rows = 0;     // remote send rows (NCCL mode)
+  uint16_t* recv = nullptr;  // [cap_rows][H]
+  uint16_t* hbuf = nullptr;  // [cap_rows][F]
+  uint16_t* ybuf = nullptr;  // [cap_rows][H]
+  uint16_t* sendbuf = nullptr;  // [send_rows][H]
+  uint16_t* retbuf = nullptr;   // [send_rows][H]
+  alignas(64) uint8_t tmA1[128];  // A of GEMM1: recv [cap][H]
+  alignas(64) uint8_t tmA2[128];  // A of GEMM2: hbuf [cap][F]
+  alignas(64) uint8_t tmB1[128];
+  alignas(64) uint8_t tmB2[128];
+  const void* tmB1_ptr = nullptr;
+  const void* tmB2_ptr = nullptr;
+  int tmB_nw = -1;
+
+  // optional K5/K6 timing events
+  bool timing = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+
+  // last dispatch
+  bool have_plan = false;
+  int last_T = 0, last_k = 0, last_tiles = 0;
+  int n_hosted = 0;
+  std::vector<int32_t> cnt_host;  // [G][E] (NCCL mode)
+};
+
+static thread_local std::string g_err;
+
+static moe_status fail(moe_ctx_t c, moe_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  g_err = buf;
+  return s;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(call)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess) return fail(ctx, MOE_ERR_NCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+#define LAUNCHED(ctx, n)                                                                  \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e_)); \
+    (ctx)->launches += (n);                                                               \
+  } while (0)
+
+static PlanBuffers plan_buffers(moe_ctx_t c) {
+  PlanBuffers b;
+  b.P = c->P_dev;
+  b.tile_hist = c->tile_hist;
+  b.tile_base = c->tile_base;
+  b.cnt_local = c->cnt_local;
+  b.cnt_all = c->virt || c->G == 1 ? c->cnt_local : c->cnt_all;
+  b.base_row = c->base_row;
+  b.seg_meta = c->seg_meta;
+  b.row_of_item = c->row_of_item;
+  b.err = c->err_dev;
+  return b;
+}
+
+static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
+  PlanArgs a;
+  a.T = T;
+  a.k = k;
+  a.E = c->E;
+  a.H = c->H;
+  a.V = c->V;
+  a.G = c->G;
+  a.me = c->me;
+  a.virt = c->virt;
+  a.n_tiles = plan_tiles(T, c->V);
+  return a;
+}
+
+extern "C" {
+
+int32_t moe_abi_version(void) { return MOE_ABI_VERSION; }
+
+const char* moe_status_str(moe_status s) {
+  switch (s) {
+    case MOE_OK: return "MOE_OK";
+    case MOE_ERR_INVALID_ARG: return "MOE_ERR_INVALID_ARG";
+    case MOE_ERR_CUDA: return "MOE_ERR_CUDA";
+    case MOE_ERR_NCCL: return "MOE_ERR_NCCL";
+    case MOE_ERR_CAPACITY: return "MOE_ERR_CAPACITY";
+    case MOE_ERR_UNSUPPORTED: return "MOE_ERR_UNSUPPORTED";
+    case MOE_ERR_DEVICE: return "MOE_ERR_DEVICE";
+    case MOE_ERR_TIMEOUT: return "MOE_ERR_TIMEOUT";
+  }
+  return "MOE_ERR_UNKNOWN";
+}
+
+const char* moe_last_error(moe_ctx_t ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int64_t moe_kernel_launches(moe_ctx_t ctx) { return ctx ? ctx->launches : 0; }
+
+moe_status moe_get_unique_id(uint8_t out[128]) {
+  moe_ctx_t ctx = nullptr;
+  if (!out) return fail(ctx, MOE_ERR_INVALID_ARG, "out is NULL");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl unique id size");
+  memcpy(out, &id, 128);
+  return MOE_OK;
+}
+
+moe_status moe_placement_contiguous(int32_t E, int32_t G, int32_t* out) {
+  moe_ctx_t ctx = nullptr;
+  if (!out || E <= 0 || G <= 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  if (E % G != 0) return fail(ctx, MOE_ERR_INVALID_ARG, "E %% G != 0 (E=%d, G=%d)", E, G);
+  const int per = E / G;
+  for (int e = 0; e < E; ++e) out[e] = e / per;
+  return MOE_OK;
+}
+
+moe_status moe_layout_host(int32_t E, int32_t G, const int32_t* P, const int32_t* cnt, int32_t* seg_start,
+                           int32_t* recv_base, int32_t* recv_rows, int32_t* send_base) {
+  moe_ctx_t ctx = nullptr;
+  if (E <= 0 || G <= 0 || !P || !cnt) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  for (int e = 0; e < E; ++e)
+    if (P[e] < 0 || P[e] >= G) return fail(ctx, MOE_ERR_INVALID_ARG, "placement value out of range");
+  std::vector<int64_t> start(E, 0);
+  for (int g = 0; g < G; ++g) {
+    int64_t acc = 0, unp = 0;
+    for (int e = 0; e < E; ++e) {
+      if (P[e] != g) continue;
+      int64_t rows = 0;
+      for (int s = 0; s < G; ++s) rows += cnt[s * E + e];
+      start[e] = acc;
+      acc += (rows + kSegAlign - 1) / kSegAlign * kSegAlign;
+      unp += rows;
+    }
+    if (recv_rows) recv_rows[g] = (int32_t)unp;
+  }
+  for (int e = 0; e < E; ++e) {
+    if (seg_start) seg_start[e] = (int32_t)start[e];
+    int64_t acc = start[e];
+    for (int s = 0; s < G; ++s) {
+      if (recv_base) recv_base[s * E + e] = (int32_t)acc;
+      acc += cnt[s * E + e];
+    }
+  }
+  if (send_base) {
+    // full send order of source s: key (P[e], e)
+    for (int s = 0; s < G; ++s) {
+      int64_t acc = 0;
+      for (int g = 0; g < G; ++g)
+        for (int e = 0; e < E; ++e)
+          if (P[e] == g) {
+            send_base[s * E + e] = (int32_t)acc;
+            acc += cnt[s * E + e];
+          }
+    }
+  }
+  return MOE_OK;
+}
+
+moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out) {
+  moe_ctx_t ctx = nullptr;
+  if (!cfg || !out) return fail(ctx, MOE_ERR_INVALID_ARG, "cfg/out is NULL");
+  const moe_config& c = *cfg;
+  if (c.hidden <= 0 || c.hidden % 64) return fail(ctx, MOE_ERR_UNSUPPORTED, "hidden must be a positive multiple of 64");
+  if (c.ffn <= 0 || c.ffn % 64) return fail(ctx, MOE_ERR_UNSUPPORTED, "ffn must be a positive multiple of 64");
+  if (c.num_experts < 1 || c.num_experts > kMaxExperts)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "num_experts must be in [1, %d]", kMaxExperts);
+  if (c.max_k < 1 || c.max_k > c.num_experts || c.max_k > kMaxK)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "max_k must be in [1, min(E, %d)]", kMaxK);
+  if (c.max_tokens < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "max_tokens < 0");
+  if (c.world < 1 || c.world > kMaxWorld || c.rank < 0 || c.rank >= c.world)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "bad world/rank");
+  if (c.virtual_ranks > 1 && c.world != 1) return fail(ctx, MOE_ERR_INVALID_ARG, "virtual_ranks needs world == 1");
+  if (c.virtual_ranks > kMaxWorld) return fail(ctx, MOE_ERR_INVALID_ARG, "virtual_ranks > %d", kMaxWorld);
+  if (c.a2a_mode != MOE_A2A_NCCL) return fail(ctx, MOE_ERR_UNSUPPORTED, "only a2a_mode = MOE_A2A_NCCL is implemented");
+  if (c.world > 1 && !uid) return fail(ctx, MOE_ERR_INVALID_ARG, "uid required when world > 1");
+
+  ctx = new moe_ctx();
+  ctx->cfg = c;
+  ctx->E = c.num_experts;
+  ctx->H = c.hidden;
+  ctx->F = c.ffn;
+  ctx->virt = c.virtual_ranks > 1;
+  ctx->G = ctx->virt ? c.virtual_ranks : c.world;
+  ctx->V = ctx->virt ? c.virtual_ranks : 1;
+  ctx->me = ctx->virt ? 0 : c.rank;
+  auto bail = [&](moe_status s) {
+    std::string m = ctx->err;
+    moe_ctx_destroy(ctx);
+    fail(nullptr, s, "%s", m.c_str());
+    return s;
+  };
+  if (cudaSetDevice(c.device) != cudaSuccess) {
+    fail(ctx, MOE_ERR_CUDA, "cudaSetDevice(%d) failed", c.device);
+    return bail(MOE_ERR_CUDA);
+  }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c.device);
+  if (major != 10) {
+    fail(ctx, MOE_ERR_UNSUPPORTED, "libmoe needs an sm_100 (B200) device, got compute capability %d.x", major);
+    return bail(MOE_ERR_UNSUPPORTED);
+  }
+  const int E = ctx->E, G = ctx->G, k = c.max_k;
+  const int64_t Tm = c.max_tokens;
+  // receive layout capacity (dropless, reading G6)
+  int64_t rows;
+  if (ctx->virt || G == 1) rows = Tm * k;
+  else rows = (int64_t)G * Tm * k;  // every source may send all its items here
+  ctx->cap_rows = rows + (int64_t)E * kSegAlign;
+  ctx->send_rows = (!ctx->virt && G > 1) ? Tm * k : 0;
+  ctx->max_tiles = plan_tiles((int)Tm, ctx->V) + ctx->V;
+
+  auto A = [&](void** p, size_t bytes) -> bool {
+    if (bytes == 0) bytes = 16;
+    if (cudaMalloc(p, bytes) != cudaSuccess) {
+      fail(ctx, MOE_ERR_CUDA, "cudaMalloc(%zu) failed", bytes);
+      return false;
+    }
+    return true;
+  };
+  bool ok = A((void**)&ctx->P_dev, sizeof(int32_t) * E) &&
+            A((void**)&ctx->tile_hist, sizeof(int32_t) * (size_t)ctx->max_tiles * E) &&
+            A((void**)&ctx->tile_base, sizeof(int32_t) * (size_t)ctx->max_tiles * E) &&
+            A((void**)&ctx->cnt_local, sizeof(int32_t) * (size_t)ctx->V * E) &&
+            A((void**)&ctx->cnt_all, sizeof(int32_t) * (size_t)G * E) &&
+            A((void**)&ctx->base_row, sizeof(int32_t) * (size_t)ctx->V * E) &&
+            A((void**)&ctx->seg_meta, sizeof(int32_t) * (size_t)(1 + 3 * E + 4)) &&
+            A((void**)&ctx->row_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
+            A((void**)&ctx->err_dev, sizeof(int)) &&
+            A((void**)&ctx->recv, (size_t)ctx->cap_rows * c.hidden * 2) &&
+            A((void**)&ctx->hbuf, (size_t)ctx->cap_rows * c.ffn * 2) &&
+            A((void**)&ctx->ybuf, (size_t)ctx->cap_rows * c.hidden * 2) &&
+            A((void**)&ctx->sendbuf, (size_t)ctx->send_rows * c.hidden * 2) &&
+            A((void**)&ctx->retbuf, (size_t)ctx->send_rows * c.hidden * 2);
+  if (!ok) return bail(MOE_ERR_CUDA);
+  cudaMemset(ctx->err_dev, 0, sizeof(int));
+  cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
+  if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess) {
+    fail(ctx, MOE_ERR_CUDA, "cudaMallocHost failed");
+    return bail(MOE_ERR_CUDA);
+  }
+  ctx->P_host.assign(E, -1);
+  ctx->cnt_host.assign((size_t)G * E, 0);
+  // A-operand tensor maps over the context-owned activation buffers
+  if (!make_tmap_2d(ctx->tmA1, ctx->recv, ctx->cap_rows, c.hidden, 128) ||
+      !make_tmap_2d(ctx->tmA2, ctx->hbuf, ctx->cap_rows, c.ffn, 128)) {
+    fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
+    return bail(MOE_ERR_CUDA);
+  }
+  if (!ctx->virt && G > 1) {
+    ncclUniqueId id;
+    memcpy(&id, uid, 128);
+    ncclResult_t r = ncclCommInitRank(&ctx->comm, G, id, c.rank);
+    if (r != ncclSuccess) {
+      fail(ctx, MOE_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+      return bail(MOE_ERR_NCCL);
+    }
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    fail(ctx, MOE_ERR_CUDA, "device sync after create failed");
+    return bail(MOE_ERR_CUDA);
+  }
+  *out = ctx;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_destroy(moe_ctx_t ctx) {
+  if (!ctx) return MOE_OK;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  if (ctx->comm) {
+    ncclCommFinalize(ctx->comm);
+    ncclCommDestroy(ctx->comm);
+  }
+  void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
+                 ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
+                 ctx->retbuf};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->P_pinned) cudaFreeHost(ctx->P_pinned);
+  if (ctx->cnt_pinned) cudaFreeHost(ctx->cnt_pinned);
+  delete ctx;
+  return MOE_OK;
+}
+
+static moe_status check_device_error(moe_ctx_t ctx) {
+  int e = 0;
+  CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  if (e) {
+    cudaMemset(ctx->err_dev, 0, sizeof(int));
+    return fail(ctx, MOE_ERR_DEVICE, "device error latched:%s%s", (e & kErrBadExpert) ? " expert id out of range" : "",
+                (e & kErrCapacity) ? " receive capacity exceeded" : "");
+  }
+  return MOE_OK;
+}
+
+moe_status moe_ctx_sync(moe_ctx_t ctx) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaStreamSynchronize(ctx->last_stream));
+  return check_device_error(ctx);
+}
+
+moe_status moe_route(moe_ctx_t ctx, const float* logits, int32_t T, int32_t E, int32_t k, int32_t* idx, float* w,
+                     moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
+  if (E != ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "E=%d != context E=%d", E, ctx->E);
+  if (k < 1 || k > E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
+  if (T > 0 && (!logits || !idx || !w)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  if (T == 0) return MOE_OK;
+  launch_route(logits, T, E, k, idx, w, s);
+  LAUNCHED(ctx, 1);
+  return MOE_OK;
+}
+
+moe_status moe_route_stats(moe_ctx_t ctx, const int32_t* idx_l, const int32_t* idx_l1, int32_t T, int32_t E,
+                           int32_t k, int64_t* load, int64_t* coact, moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
+  if (E != ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "E=%d != context E=%d", E, ctx->E);
+  if (E > 128) return fail(ctx, MOE_ERR_UNSUPPORTED, "route_stats supports E <= 128");
+  if (k < 1 || k > E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
+  if (T > 0 && (!idx_l || !load)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  if (idx_l1 && !coact) return fail(ctx, MOE_ERR_INVALID_ARG, "coact is NULL but idx_l1 is given");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  if (T == 0) return MOE_OK;
+  launch_route_stats(idx_l, idx_l1, T, E, k, load, coact, ctx->err_dev, ctx->num_sms, s);
+  LAUNCHED(ctx, 1);
+  return MOE_OK;
+}
+
+moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E, moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (E != ctx->E || !load) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  if (!ctx->comm) return MOE_OK;
+  NC(ncclGroupStart());
+  NC(ncclAllReduce(load, load, E, ncclInt64, ncclSum, ctx->comm, s));
+  if (coact) NC(ncclAllReduce(coact, coact, (size_t)E * E, ncclInt64, ncclSum, ctx->comm, s));
+  NC(ncclGroupEnd());
+  return MOE_OK;
+}
+
+moe_status moe_pack_w13(const moe_bf16* w1, const moe_bf16* w3, int32_t n, int32_t F, int32_t H, moe_bf16* w13,
+                        moe_stream_t stream) {
+  moe_ctx_t ctx = nullptr;
+  if (!w1 || !w3 || !w13 || n < 0 || F <= 0 || H <= 0 || F % 64 || H % 64)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments (F, H multiples of 64)");
+  if (n == 0) return MOE_OK;
+  launch_pack_w13(w1, w3, n, F, H, w13, (cudaStream_t)stream);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
+  return MOE_OK;
+}
+
+moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
+                        const int32_t* expert_to_rank, moe_dispatch_info* info, moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
+  if (k < 1 || k > ctx->E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
+  if (!expert_to_rank) return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank is NULL");
+  if (T > 0 && (!x || !idx)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  const int E = ctx->E, G = ctx->G, H = ctx->H;
+  for (int e = 0; e < E; ++e)
+    if (expert_to_rank[e] < 0 || expert_to_rank[e] >= G)
+      return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank[%d]=%d outside [0, %d)", e, expert_to_rank[e], G);
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  CU(cudaSetDevice(ctx->cfg.device));
+  if (!ctx->P_valid || memcmp(ctx->P_host.data(), expert_to_rank, sizeof(int32_t) * E) != 0) {
+    CU(cudaStreamSynchronize(s));  // the pinned staging copy may still be in flight
+    memcpy(ctx->P_pinned, expert_to_rank, sizeof(int32_t) * E);
+    memcpy(ctx->P_host.data(), expert_to_rank, sizeof(int32_t) * E);
+    CU(cudaMemcpyAsync(ctx->P_dev, ctx->P_pinned, sizeof(int32_t) * E, cudaMemcpyHostToDevice, s));
+    ctx->P_valid = true;
+  }
+  int n_hosted = 0;
+  for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->me);
+  ctx->n_hosted = n_hosted;
+
+  PlanArgs a = plan_args(ctx, T, k);
+  PlanBuffers b = plan_buffers(ctx);
+  launch_count(a, idx, b, s);
+  launch_scan(a, b, s);
+  LAUNCHED(ctx, (a.n_tiles > 0) + 1);
+  const bool nccl = ctx->comm != nullptr;
+  if (nccl) {
+    NC(ncclAllGather(ctx->cnt_local, ctx->cnt_all, E, ncclInt32, ctx->comm, s));
+    CU(cudaMemcpyAsync(ctx->cnt_pinned, ctx->cnt_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    memcpy(ctx->cnt_host.data(), ctx->cnt_pinned, sizeof(int32_t) * G * E);
+  }
+  launch_layout(a, b, ctx->cap_rows, s);
+  launch_scatter(a, x, idx, b, ctx->recv, ctx->sendbuf, s);
+  LAUNCHED(ctx, 1 + (a.n_tiles > 0));
+  if (nccl) {
+    const int32_t* P = ctx->P_host.data();
+    const int32_t* cnt = ctx->cnt_host.data();
+    std::vector<int32_t> recv_base((size_t)G * E);
+    moe_layout_host(E, G, P, cnt, nullptr, recv_base.data(), nullptr, nullptr);
+    NC(ncclGroupStart());
+    // sends: remote experts in key (P[e], e) order; compact send buffer
+    int64_t off = 0;
+    for (int g = 0; g < G; ++g) {
+      if (g == ctx->me) continue;
+      for (int e = 0; e < E; ++e) {
+        if (P[e] != g) continue;
+        const int64_t n = cnt[ctx->me * E + e];
+        if (n) NC(ncclSend(ctx->sendbuf + off * H, (size_t)n * H, ncclBfloat16, g, ctx->comm, s));
+        off += n;
+      }
+    }
+    for (int src = 0; src < G; ++src) {
+      if (src == ctx->me) continue;
+      for (int e = 0; e < E; ++e) {
+        if (P[e] != ctx->me) continue;
+        const int64_t n = cnt[src * E + e];
+        if (n)
+          NC(ncclRecv(ctx->recv + (int64_t)recv_base[src * E + e] * H, (size_t)n * H, ncclBfloat16, src, ctx->comm, s));
+      }
+    }
+    NC(ncclGroupEnd());
+  }
+  ctx->have_plan = true;
+  ctx->last_T = T;
+  ctx->last_k = k;
+  ctx->last_tiles = a.n_tiles;
+  if (info) {
+    memset(info, 0, sizeof *info);
+    CU(cudaStreamSynchronize(s));
+    std::vector<int32_t> cnt((size_t)G * E);
+    CU(cudaMemcpy(cnt.data(), b.cnt_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost));
+    info->world = G;
+    info->num_local_experts = n_hosted;
+    int64_t rr = 0;
+    for (int g = 0; g < G && g < 64; ++g) {
+      int64_t r = 0;
+      for (int src = 0; src < G; ++src)
+        for (int e = 0; e < E; ++e)
+          if (expert_to_rank[e] == g) r += cnt[src * E + e];
+      info->recv_counts[g] = (int32_t)r;
+      if (ctx->virt || g == ctx->me) rr += r;
+    }
+    if (!ctx->virt)
+      for (int g = 0; g < G && g < 64; ++g) {
+        int64_t sc = 0;
+        for (int e = 0; e < E; ++e)
+          if (expert_to_rank[e] == g) sc += cnt[ctx->me * E + e];
+        info->send_counts[g] = (int32_t)sc;
+      }
+    info->recv_rows = rr;
+  }
+  return MOE_OK;
+}
+
+moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2, moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_expert_ffn before moe_dispatch");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  const int nw = ctx->n_hosted;
+  if (nw == 0) return MOE_OK;
+  if (!w13 || !w2) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL weights");
+  const int H = ctx->H, F = ctx->F;
+  const int nw_rows = ctx->virt ? ctx->E : nw;
+  if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows) {
+    const int bn1 = gemm_block_n(2 * F, true), bn2 = gemm_block_n(H, false);
+    if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)nw_rows * 2 * F, H, bn1) ||
+        !make_tmap_2d(ctx->tmB2, w2, (uint64_t)nw_rows * H, F, bn2))
+      return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weights");
+    ctx->tmB1_ptr = w13;
+    ctx->tmB2_ptr = w2;
+    ctx->tmB_nw = nw_rows;
+  }
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[0], s));
+  cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
+                                      ctx->num_sms, s);
+  if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[1], s));
+  e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms, s);
+  if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
+  if (ctx->timing) CU(cudaEventRecord(ctx->ev[2], s));
+  ctx->launches += 2;
+  return MOE_OK;
+}
+
+moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t enable) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  CU(cudaSetDevice(ctx->cfg.device));
+  for (auto& e : ctx->ev)
+    if (!e) CU(cudaEventCreate(&e));
+  ctx->timing = enable != 0;
+  return MOE_OK;
+}
+
+moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms) {
+  if (!ctx || !ms) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  if (!ctx->ev[2]) return fail(ctx, MOE_ERR_INVALID_ARG, "timing was never enabled");
+  CU(cudaEventSynchronize(ctx->ev[2]));
+  CU(cudaEventElapsedTime(&ms[0], ctx->ev[0], ctx->ev[1]));
+  CU(cudaEventElapsedTime(&ms[1], ctx->ev[1], ctx->ev[2]));
+  return MOE_OK;
+}
+
+moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
+  if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  CU(cudaMemcpyAsync(ctx->ybuf, ctx->recv, (size_t)ctx->cap_rows * ctx->H * 2, cudaMemcpyDeviceToDevice, s));
+  return MOE_OK;
+}
+
+moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_combine before moe_dispatch");
+  if (ctx->last_T > 0 && (!w || !out)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  const int E = ctx->E, G = ctx->G, H = ctx->H;
+  if (ctx->comm) {
+    const int32_t* P = ctx->P_host.data();
+    const int32_t* cnt = ctx->cnt_host.data();
+    std::vector<int32_t> recv_base((size_t)G * E);
+    moe_layout_host(E, G, P, cnt, nullptr, recv_base.data(), nullptr, nullptr);
+    NC(ncclGroupStart());
+    for (int src = 0; src < G; ++src) {
+      if (src == ctx->me) continue;
+      for (int e = 0; e < E; ++e) {
+        if (P[e] != ctx->me) continue;
+        const int64_t n = cnt[src * E + e];
+        if (n)
+          NC(ncclSend(ctx->ybuf + (int64_t)recv_base[src * E + e] * H, (size_t)n * H, ncclBfloat16, src, ctx->comm, s));
+      }
+    }
+    int64_t off = 0;
+    for (int g = 0; g < G; ++g) {
+      if (g == ctx->me) continue;
+      for (int e = 0; e < E; ++e) {
+        if (P[e] != g) continue;
+        const int64_t n = cnt[ctx->me * E + e];
+        if (n) NC(ncclRecv(ctx->retbuf + off * H, (size_t)n * H, ncclBfloat16, g, ctx->comm, s));
+        off += n;
+      }
+    }
+    NC(ncclGroupEnd());
+  }
+  PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
+  PlanBuffers b = plan_buffers(ctx);
+  launch_combine(a, w, b, ctx->ybuf, ctx->retbuf, out, s);
+  LAUNCHED(ctx, a.n_tiles > 0);
+  return MOE_OK;
+}
+
+// Decode the device plan into the oracle's C3 terms (unpadded receive position
+// on the destination rank, source send-order slot).
+moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, int32_t* send_slot, int32_t* cnt_out) {
+  if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaStreamSynchronize(ctx->last_stream));
+  moe_status st = check_device_error(ctx);
+  if (st != MOE_OK) return st;
+  const int E = ctx->E, G = ctx->G, T = ctx->last_T, k = ctx->last_k;
+  std::vector<int32_t> cnt((size_t)G * E), rows((size_t)std::max(1, T * k));
+  const int32_t* cnt_dev = (ctx->virt || G == 1) ? ctx->cnt_local : ctx->cnt_all;
+  CU(cudaMemcpy(cnt.data(), cnt_dev, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost));
+  if (T * k) CU(cudaMemcpy(rows.data(), ctx->row_of_item, sizeof(int32_t) * T * k, cudaMemcpyDeviceToHost));
+  if (cnt_out) memcpy(cnt_out, cnt.data(), sizeof(int32_t) * G * E);
+  const int32_t* P = ctx->P_host.data();
+  // unpadded receive start of (e, s) on rank P[e]; send-order base of (s, e)
+  std::vector<int64_t> ustart((size_t)G * E), sbase((size_t)G * E), cbase(E);
+  for (int g = 0; g < G; ++g) {
+    int64_t acc = 0;
+    for (int e = 0; e < E; ++e) {
+      if (P[e] != g) continue;
+      for (int s = 0; s < G; ++s) {
+        ustart[(size_t)s * E + e] = acc;
+        acc += cnt[(size_t)s * E + e];
+      }
+    }
+  }
+  for (int s = 0; s < G; ++s) {
+    int64_t acc = 0;
+    for (int g = 0; g < G; ++g)
+      for (int e = 0; e < E; ++e)
+        if (P[e] == g) {
+          sbase[(size_t)s * E + e] = acc;
+          acc += cnt[(size_t)s * E + e];
+        }
+  }
+  // padded device receive base of (s, e): virtual mode concatenates every rank's
+  // segments in key (P[e], e) order; real mode uses this rank's own buffer.
+  std::vector<int64_t> pstart((size_t)G * E, 0);
+  {
+    std::vector<int> order(E);
+    for (int e = 0; e < E; ++e) order[e] = e;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return P[x] < P[y]; });
+    int64_t acc = 0;
+    for (int e : order) {
+      if (!(ctx->virt || P[e] == ctx->me)) continue;
+      int64_t r = 0;
+      for (int s = 0; s < G; ++s) {
+        pstart[(size_t)s * E + e] = acc + r;
+        r += cnt[(size_t)s * E + e];
+      }
+      acc += (r + kSegAlign - 1) / kSegAlign * kSegAlign;
+    }
+  }
+  // compact send base (remote experts only) of this rank
+  std::vector<int64_t> rbase(E, 0);
+  {
+    int64_t acc = 0;
+    for (int g = 0; g < G; ++g)
+      for (int e = 0; e < E; ++e)
+        if (P[e] == g && !(ctx->virt || g == ctx->me)) {
+          rbase[e] = acc;
+          acc += cnt[(size_t)ctx->me * E + e];
+        }
+  }
+  // expert of each item is needed to decode; reconstruct from the row ranges
+  for (int t = 0; t < T; ++t) {
+    int s = ctx->virt ? 0 : ctx->me;
+    if (ctx->virt) {
+      const int base = T / G, rem = T % G;
+      int acc = 0;
+      for (s = 0; s < G; ++s) {
+        const int n = base + (s < rem ? 1 : 0);
+        if (t < acc + n) break;
+        acc += n;
+      }
+    }
+    for (int j = 0; j < k; ++j) {
+      const int32_t v = rows[(size_t)t * k + j];
+      int32_t dr = -1, rp = -1, ss = -1;
+      if (v != -1) {
+        const bool remote = v < -1;
+        const int64_t row = remote ? -(int64_t)v - 2 : v;
+        // find the expert whose range contains the row
+        for (int e = 0; e < E; ++e) {
+          const int64_t n = cnt[(size_t)s * E + e];
+          if (n == 0) continue;
+          const int64_t b0 = remote ? rbase[e] : pstart[(size_t)s * E + e];
+          if (remote == !(ctx->virt || P[e] == ctx->me) && row >= b0 && row < b0 + n) {
+            const int64_t rank_within = row - b0;
+            dr = P[e];
+            rp = (int32_t)(ustart[(size_t)s * E + e] + rank_within);
+            ss = (int32_t)(sbase[(size_t)s * E + e] + rank_within);
+            break;
+          }
+        }
+      }
+      if (dest_rank) dest_rank[(size_t)t * k + j] = dr;
+      if (recv_pos) recv_pos[(size_t)t * k + j] = rp;
+      if (send_slot) send_slot[(size_t)t * k + j] = ss;
+    }
+  }
+  return MOE_OK;
+}
+
+moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out) {
+  if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaStreamSynchronize(ctx->last_stream));
+  const int E = ctx->E, H = ctx->H;
+  std::vector<int32_t> meta(1 + 3 * E + 4);
+  CU(cudaMemcpy(meta.data(), ctx->seg_meta, sizeof(int32_t) * meta.size(), cudaMemcpyDeviceToHost));
+  const int nseg = meta[0];
+  int64_t out = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const int64_t r0 = meta[1 + i], n = meta[1 + E + i];
+    if (rows_host && out + n <= max_rows && n > 0)
+      CU(cudaMemcpy(rows_host + out * H, ctx->recv + r0 * H, (size_t)n * H * 2, cudaMemcpyDeviceToHost));
+    out += n;
+  }
+  if (rows_out) *rows_out = out;
+  if (rows_host && out > max_rows) return fail(ctx, MOE_ERR_CAPACITY, "max_rows too small (%lld)", (long long)out);
+  return MOE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,255 @@
+"""Thin ctypes binding of libmoe (include/moe.h).  Argument marshalling only:
+every step of the layer runs in the library's sm_100a kernels.  Torch supplies
+device memory, streams and (for world > 1) the broadcast of the NCCL unique id.
+
+There is no fallback: if libmoe.so is missing or fails to load, importing this
+module raises.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmoe.so")
+
+MOE_OK = 0
+STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_CUDA", 3: "MOE_ERR_NCCL", 4: "MOE_ERR_CAPACITY",
+          5: "MOE_ERR_UNSUPPORTED", 6: "MOE_ERR_DEVICE", 7: "MOE_ERR_TIMEOUT"}
+
+# Every symbol include/moe.h declares (checked by tests/test_abi_cpu.py).
+EXPORTS = ["moe_get_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_sync", "moe_status_str",
+           "moe_last_error", "moe_abi_version", "moe_route", "moe_route_stats", "moe_stats_allreduce",
+           "moe_dispatch", "moe_expert_ffn", "moe_combine", "moe_pack_w13", "moe_placement_contiguous",
+           "moe_layout_host", "moe_debug_plan", "moe_debug_identity_ffn", "moe_debug_recv", "moe_kernel_launches",
+           "moe_ffn_timing_enable", "moe_ffn_timing_read"]
+
+
+class MoeError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("max_tokens", ctypes.c_int32), ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("num_experts", ctypes.c_int32), ("max_k", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("device", ctypes.c_int32), ("virtual_ranks", ctypes.c_int32),
+                ("a2a_mode", ctypes.c_int32)]
+
+
+class DispatchInfo(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("num_local_experts", ctypes.c_int32), ("recv_rows", ctypes.c_int64),
+                ("send_counts", ctypes.c_int32 * 64), ("recv_counts", ctypes.c_int32 * 64)]
+
+
+def load_library(path=LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(f"libmoe.so not found at {path}: build it with "
+                          f"`python -m paper_2502_06643_b200.build` (no fallback path exists)")
+    lib = ctypes.CDLL(path)
+    P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "moe_get_unique_id": [P],
+        "moe_ctx_create": [ctypes.POINTER(Config), P, ctypes.POINTER(P)],
+        "moe_ctx_destroy": [P],
+        "moe_ctx_sync": [P],
+        "moe_route": [P, P, I32, I32, I32, P, P, P],
+        "moe_route_stats": [P, P, P, I32, I32, I32, P, P, P],
+        "moe_stats_allreduce": [P, P, P, I32, P],
+        "moe_dispatch": [P, P, P, I32, I32, P, P, P],
+        "moe_expert_ffn": [P, P, P, P],
+        "moe_combine": [P, P, P, P],
+        "moe_pack_w13": [P, P, I32, I32, I32, P, P],
+        "moe_placement_contiguous": [I32, I32, P],
+        "moe_layout_host": [I32, I32, P, P, P, P, P, P],
+        "moe_debug_plan": [P, P, P, P, P],
+        "moe_debug_identity_ffn": [P, P],
+        "moe_debug_recv": [P, P, I64, P],
+        "moe_ffn_timing_enable": [P, I32],
+        "moe_ffn_timing_read": [P, P],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.moe_status_str.argtypes = [ctypes.c_int]
+    lib.moe_status_str.restype = ctypes.c_char_p
+    lib.moe_last_error.argtypes = [P]
+    lib.moe_last_error.restype = ctypes.c_char_p
+    lib.moe_abi_version.restype = ctypes.c_int32
+    lib.moe_kernel_launches.argtypes = [P]
+    lib.moe_kernel_launches.restype = ctypes.c_int64
+    return lib
+
+
+_lib = load_library()
+
+
+def lib():
+    return _lib
+
+
+def _check(status, ctx=None):
+    if status != MOE_OK:
+        msg = _lib.moe_last_error(ctx).decode(errors="replace")
+        raise MoeError(status, msg)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def placement_contiguous(E, G):
+    out = np.zeros(E, dtype=np.int32)
+    _check(_lib.moe_placement_contiguous(E, G, _np_ptr(out)))
+    return out
+
+
+def layout_host(P, cnt):
+    """Host layout (see moe_layout_host): returns seg_start, recv_base, recv_rows, send_base."""
+    P = np.ascontiguousarray(P, dtype=np.int32)
+    cnt = np.ascontiguousarray(cnt, dtype=np.int32)
+    G, E = cnt.shape
+    seg = np.zeros(E, np.int32)
+    rb = np.zeros((G, E), np.int32)
+    rr = np.zeros(G, np.int32)
+    sb = np.zeros((G, E), np.int32)
+    _check(_lib.moe_layout_host(E, G, _np_ptr(P), _np_ptr(cnt), _np_ptr(seg), _np_ptr(rb), _np_ptr(rr), _np_ptr(sb)))
+    return seg, rb, rr, sb
+
+
+def get_unique_id():
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_lib.moe_get_unique_id(buf))
+    return bytes(buf)
+
+
+def pack_w13(w1, w3, stream=None):
+    """w1, w3: bf16 [n][F][H] on the device -> w13 [n][2F][H] (moe_pack_w13)."""
+    n, F, H = w1.shape
+    w13 = torch.empty(n, 2 * F, H, dtype=torch.bfloat16, device=w1.device)
+    _check(_lib.moe_pack_w13(_ptr(w1), _ptr(w3), n, F, H, _ptr(w13), _stream(stream)))
+    return w13
+
+
+class MoeLayer:
+    """One libmoe context (one EP rank, or G virtual ranks on one GPU)."""
+
+    def __init__(self, *, max_tokens, hidden, ffn, num_experts, max_k, world=1, rank=0, device=0,
+                 virtual_ranks=1, uid=None):
+        self.cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, world, rank, device, virtual_ranks, 0)
+        self.E, self.H, self.F = num_experts, hidden, ffn
+        self.G = virtual_ranks if virtual_ranks > 1 else world
+        self.device = torch.device("cuda", device)
+        h = ctypes.c_void_p()
+        uid_buf = None
+        if uid is not None:
+            uid_buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(_lib.moe_ctx_create(ctypes.byref(self.cfg), uid_buf, ctypes.byref(h)))
+        self._ctx = h
+        self._last = None
+
+    def close(self):
+        if self._ctx:
+            _lib.moe_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _c(self, status):
+        _check(status, self._ctx)
+
+    @property
+    def kernel_launches(self):
+        return int(_lib.moe_kernel_launches(self._ctx))
+
+    def ffn_timing(self, enable=True):
+        self._c(_lib.moe_ffn_timing_enable(self._ctx, 1 if enable else 0))
+
+    def ffn_timing_read(self):
+        ms = (ctypes.c_float * 2)()
+        self._c(_lib.moe_ffn_timing_read(self._ctx, ms))
+        return float(ms[0]), float(ms[1])
+
+    def sync(self):
+        self._c(_lib.moe_ctx_sync(self._ctx))
+
+    # a1
+    def route(self, logits, k, idx=None, w=None, stream=None):
+        T, E = logits.shape
+        if idx is None:
+            idx = torch.empty(T, k, dtype=torch.int32, device=logits.device)
+        if w is None:
+            w = torch.empty(T, k, dtype=torch.float32, device=logits.device)
+        self._c(_lib.moe_route(self._ctx, _ptr(logits), T, E, k, _ptr(idx), _ptr(w), _stream(stream)))
+        return idx, w
+
+    # a2
+    def route_stats(self, idx_l, idx_l1, load, coact, stream=None):
+        T, k = idx_l.shape
+        self._c(_lib.moe_route_stats(self._ctx, _ptr(idx_l), _ptr(idx_l1), T, self.E, k, _ptr(load), _ptr(coact),
+                                     _stream(stream)))
+
+    def stats_allreduce(self, load, coact, stream=None):
+        self._c(_lib.moe_stats_allreduce(self._ctx, _ptr(load), _ptr(coact), self.E, _stream(stream)))
+
+    # a3-a5
+    def dispatch(self, x, idx, expert_to_rank, info=False, stream=None):
+        T, k = idx.shape
+        P = np.ascontiguousarray(expert_to_rank, dtype=np.int32)
+        inf = DispatchInfo() if info else None
+        self._c(_lib.moe_dispatch(self._ctx, _ptr(x), _ptr(idx), T, k, _np_ptr(P),
+                                  ctypes.byref(inf) if inf is not None else None, _stream(stream)))
+        self._last = (T, k)
+        return inf
+
+    # a6
+    def expert_ffn(self, w13, w2, stream=None):
+        self._c(_lib.moe_expert_ffn(self._ctx, _ptr(w13), _ptr(w2), _stream(stream)))
+
+    def identity_ffn(self, stream=None):
+        self._c(_lib.moe_debug_identity_ffn(self._ctx, _stream(stream)))
+
+    # a7-a8
+    def combine(self, w, out=None, stream=None):
+        T, k = self._last
+        if out is None:
+            out = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.device)
+        self._c(_lib.moe_combine(self._ctx, _ptr(w), _ptr(out), _stream(stream)))
+        return out
+
+    # debug views
+    def debug_plan(self):
+        T, k = self._last
+        dr = np.zeros((T, k), np.int32)
+        rp = np.zeros((T, k), np.int32)
+        ss = np.zeros((T, k), np.int32)
+        cnt = np.zeros((self.G, self.E), np.int32)
+        self._c(_lib.moe_debug_plan(self._ctx, _np_ptr(dr), _np_ptr(rp), _np_ptr(ss), _np_ptr(cnt)))
+        return dr, rp, ss, cnt
+
+    def debug_recv(self):
+        n = ctypes.c_int64()
+        self._c(_lib.moe_debug_recv(self._ctx, None, 0, ctypes.byref(n)))
+        buf = np.zeros((max(n.value, 1), self.H), np.uint16)
+        self._c(_lib.moe_debug_recv(self._ctx, _np_ptr(buf), n.value, ctypes.byref(n)))
+        return buf[:n.value]

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
+element on the same seeded inputs.
+
+Bars (BASELINE north_star): bit-exact for routing indices, permutation, per-GPU
+splits and co-activation counts; within 2e-2 (tests/_util.py, reading G16) for
+gate weights and layer outputs.  Sizes span several tiles with ragged tails;
+the full BASELINE configuration (Mixtral layer, T = 16384, the bench's launch
+configuration at N = 1) is checked on sampled tokens.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import layer as olayer
+from oracle import plan as oplan
+from oracle import route as oroute
+from oracle import stats as ostats
+from paper_2502_06643_b200 import placement
+from tests._util import Inputs, assert_close_layer, bf16_to_f64
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+def _moe():
+    from paper_2502_06643_b200 import moe
+    return moe
+
+
+def make_layer(T, H, F, E, k, G=1):
+    moe = _moe()
+    return moe.MoeLayer(max_tokens=max(T, 1), hidden=H, ffn=F, num_experts=E, max_k=k, virtual_ranks=G)
+
+
+# ------------------------------------------------------------------ a1
+@pytest.mark.parametrize("T,E,k", [(1000, 8, 2), (4096, 8, 2), (777, 4, 1), (513, 16, 4), (1031, 64, 8),
+                                   (300, 128, 16), (257, 256, 8), (65, 3, 3)])
+def test_route_bit_exact_indices(cuda_ok, T, E, k):
+    lay = make_layer(T, 64, 64, E, k)
+    logits = synth.zipf_logits(T, E, 1.2, seed=T + E)
+    # force ties and signed zeros on some rows
+    logits[::7, :2] = 0.5
+    logits[::11, 0] = 0.0
+    logits[::11, 1] = -0.0
+    logits[::13] = logits[::13].round()
+    idx, w = lay.route(logits.to(DEV), k)
+    torch.cuda.synchronize()
+    ridx, rw = oroute.route(logits.numpy(), k)
+    assert np.array_equal(idx.cpu().numpy(), ridx)
+    np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=2e-2, atol=0)
+    assert np.abs(w.cpu().numpy().astype(np.float64) - rw).max() < 1e-5
+
+
+def test_route_empty(cuda_ok):
+    lay = make_layer(16, 64, 64, 8, 2)
+    idx, w = lay.route(torch.zeros(0, 8, device=DEV), 2)
+    assert idx.shape == (0, 2)
+
+
+# ------------------------------------------------------------------ a2
+@pytest.mark.parametrize("T,E,k", [(5000, 8, 2), (1031, 64, 8), (333, 128, 4), (1, 8, 2)])
+def test_route_stats_bit_exact(cuda_ok, T, E, k):
+    lay = make_layer(T, 64, 64, E, k)
+    l0 = synth.zipf_logits(T, E, 1.6, seed=1)
+    l1 = synth.zipf_logits(T, E, 1.0, seed=2)
+    a, _ = oroute.route(l0.numpy(), k)
+    b, _ = oroute.route(l1.numpy(), k)
+    load = torch.zeros(E, dtype=torch.int64, device=DEV)
+    coact = torch.zeros(E, E, dtype=torch.int64, device=DEV)
+    ia, ib = torch.from_numpy(a).to(DEV), torch.from_numpy(b).to(DEV)
+    lay.route_stats(ia, ib, load, coact)
+    lay.route_stats(ia, ib, load, coact)          # accumulates
+    lay.sync()
+    rl, rc = ostats.route_stats(a, b, E)
+    assert np.array_equal(load.cpu().numpy(), 2 * rl)
+    assert np.array_equal(coact.cpu().numpy(), 2 * rc)
+    # idx_l1 = NULL: load only
+    load2 = torch.zeros(E, dtype=torch.int64, device=DEV)
+    lay.route_stats(ia, None, load2, None)
+    lay.sync()
+    assert np.array_equal(load2.cpu().numpy(), rl)
+
+
+def test_route_stats_bad_expert_latches_device_error(cuda_ok):
+    moe = _moe()
+    lay = make_layer(100, 64, 64, 8, 2)
+    idx = torch.zeros(100, 2, dtype=torch.int32, device=DEV)
+    idx[5, 1] = 9
+    load = torch.zeros(8, dtype=torch.int64, device=DEV)
+    lay.route_stats(idx, None, load, None)
+    with pytest.raises(moe.MoeError) as ei:
+        lay.sync()
+    assert ei.value.status == 6
+
+
+# ------------------------------------------------------------------ a3-a5
+PLACEMENTS = [
+    (1, [0] * 8),
+    (2, [0, 0, 0, 0, 1, 1, 1, 1]),
+    (4, [0, 0, 1, 1, 2, 2, 3, 3]),
+    (4, [0, 1, 2, 2, 3, 2, 3, 3]),       # ILP-1 balanced, uneven experts per rank
+    (4, [3, 3, 3, 3, 3, 3, 1, 1]),       # ranks 0 and 2 host no expert (reading G13)
+    (8, [7, 6, 5, 4, 3, 2, 1, 0]),
+]
+
+
+@pytest.mark.parametrize("G,P", PLACEMENTS)
+@pytest.mark.parametrize("T", [1000, 130])
+def test_dispatch_plan_bit_exact(cuda_ok, G, P, T):
+    E, k, H = 8, 2, 64
+    inp = Inputs(T, H, 128, E, k, s=1.6, seed=G * 100 + T, with_weights=False)
+    lay = make_layer(T, H, 128, E, k, G)
+    x, logits = inp.to_device(DEV)
+    idx, w = lay.route(logits, k)
+    info = lay.dispatch(x, idx, P, info=True)
+    dr, rp, ss, cnt = lay.debug_plan()
+    ridx, _ = oroute.route(inp.logits.numpy(), k)
+    blocks = oplan.token_blocks(T, G)
+    pl = oplan.plan([ridx[a:b] for a, b in blocks], np.array(P), G)
+    assert np.array_equal(cnt, pl["cnt"])
+    for s, (a, b) in enumerate(blocks):
+        assert np.array_equal(ss[a:b], pl["slot"][s])
+        assert np.array_equal(rp[a:b], pl["recv_pos"][s])
+        assert np.array_equal(dr[a:b], np.array(P)[ridx[a:b]])
+    assert list(info.recv_counts)[:G] == pl["recv_counts"].tolist()
+    # payload: every received row is bit-identical to its source row, in receive order
+    rows = lay.debug_recv()
+    xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+    ref = np.concatenate([xb[[blocks[s][0] + t for (s, t, j, e) in pl["recv"][g]]].reshape(-1, H)
+                          for g in range(G)])
+    assert np.array_equal(rows, ref)
+
+
+@pytest.mark.parametrize("G,P", PLACEMENTS)
+def test_identity_expert_round_trip_bit_exact(cuda_ok, G, P):
+    """dispatch -> identity expert -> combine returns x bit-exactly."""
+    T, E, k, H = 999, 8, 2, 256
+    inp = Inputs(T, H, 128, E, k, s=1.6, seed=7, with_weights=False)
+    lay = make_layer(T, H, 128, E, k, G)
+    x, logits = inp.to_device(DEV)
+    idx, w = lay.route(logits, k)
+    lay.dispatch(x, idx, P)
+    lay.identity_ffn()
+    out = lay.combine(w)
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int16), x.view(torch.int16))
+
+
+def test_empty_and_invalid_inputs(cuda_ok):
+    moe = _moe()
+    lay = make_layer(64, 64, 128, 8, 2, 4)
+    x = torch.zeros(0, 64, dtype=torch.bfloat16, device=DEV)
+    idx = torch.zeros(0, 2, dtype=torch.int32, device=DEV)
+    lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 3, 3])
+    out = lay.combine(torch.zeros(0, 2, device=DEV))
+    assert out.shape == (0, 64)
+    with pytest.raises(moe.MoeError) as ei:
+        lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 3, 4])      # placement value >= G
+    assert ei.value.status == 1
+    with pytest.raises(moe.MoeError) as ei:
+        lay.route(torch.zeros(65, 8, device=DEV), 2)          # T > max_tokens
+    assert ei.value.status == 4
+    with pytest.raises(moe.MoeError):
+        lay.route(torch.zeros(8, 8, device=DEV), 9)           # k > E
+
+
+# ------------------------------------------------------------------ a6-a8, whole layer
+def run_layer(lay, inp, P, G):
+    x, logits = inp.to_device(DEV)
+    idx, w = lay.route(logits, inp.k)
+    lay.dispatch(x, idx, P)
+    hosted = list(range(inp.E)) if G > 1 or lay.G > 1 else [e for e in range(inp.E) if P[e] == 0]
+    w1, w3, w2 = inp.device_weights(DEV, hosted)
+    moe = _moe()
+    w13 = moe.pack_w13(w1, w3)
+    lay.expert_ffn(w13, w2)
+    out = lay.combine(w)
+    lay.sync()
+    return out, idx, w
+
+
+@pytest.mark.parametrize("T,H,F,E,k,G,P", [
+    (1024, 64, 128, 8, 2, 4, [0, 0, 1, 1, 2, 2, 3, 3]),     # BASELINE configs[0] (tiny, 4 virtual ranks)
+    (1024, 64, 128, 8, 2, 4, [0, 1, 2, 2, 3, 2, 3, 3]),
+    (2000, 512, 1024, 8, 2, 1, [0] * 8),                   # several M/N/K tiles, ragged M tails
+    (1500, 256, 192, 6, 3, 2, [1, 0, 1, 1, 0, 1]),           # F % 128 != 0 -> 128-wide SwiGLU tiles
+    (700, 128, 256, 16, 4, 4, [e % 4 for e in range(16)]),
+])
+def test_layer_parity(cuda_ok, T, H, F, E, k, G, P):
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=11)
+    lay = make_layer(T, H, F, E, k, G)
+    out, idx, w = run_layer(lay, inp, P, G)
+    ref, ridx, rw = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    assert np.array_equal(idx.cpu().numpy(), ridx)
+    assert_close_layer(bf16_to_f64(out), ref)
+
+
+def test_placement_invariance_bit_exact(cuda_ok):
+    """The GEMM is deterministic (fixed K order, no split-K), so the layer output is
+    bit-identical across placements and G (SURVEY §8(c) 'Placement invariance')."""
+    T, H, F, E, k = 1200, 128, 256, 8, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=3)
+    outs = []
+    for G, P in [(1, [0] * 8), (4, [0, 0, 1, 1, 2, 2, 3, 3]), (4, [0, 1, 2, 2, 3, 2, 3, 3]), (8, list(range(8)))]:
+        lay = make_layer(T, H, F, E, k, G)
+        out, _, _ = run_layer(lay, inp, P, G)
+        outs.append(out.view(torch.int16).cpu())
+        lay.close()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_mixtral_layer_full_size_sampled(cuda_ok):
+    """BASELINE configs[1] shape at N=1 (the bench's workload: E8 k2 H4096 F14336,
+    T = 16384 tokens, all experts on one GPU), checked on sampled tokens against
+    the oracle's direct definition."""
+    T, H, F, E, k = 16384, 4096, 14336, 8, 2
+    dev = torch.device(DEV)
+    x = synth.hidden_states(T, H, seed=0, device=dev)
+    logits = synth.zipf_logits(T, E, 1.6, seed=0, device=dev)
+    ws = [synth.expert_weights(e, H, F, 0, device=dev) for e in range(E)]
+    moe = _moe()
+    lay = make_layer(T, H, F, E, k, 1)
+    idx, w = lay.route(logits, k)
+    lay.dispatch(x, idx, [0] * 8)
+    w13 = moe.pack_w13(torch.stack([q[0] for q in ws]), torch.stack([q[1] for q in ws]))
+    w2 = torch.stack([q[2] for q in ws])
+    lay.expert_ffn(w13, w2)
+    out = lay.combine(w)
+    lay.sync()
+    sel = np.array(sorted(set(np.random.default_rng(0).integers(0, T, 48).tolist()) | {0, T - 1}))
+    xs = bf16_to_f64(x[sel])
+    ls = logits[sel].cpu().numpy()
+    cache = {}
+
+    def fn(e, rows):
+        if e not in cache:
+            cache.clear()
+            cache[e] = tuple(bf16_to_f64(m) for m in ws[e])
+        from oracle import ffn
+        return ffn.swiglu(rows, *cache[e])[1]
+    ref, ridx, rw = olayer.layer_direct(xs, ls, k, fn)
+    assert np.array_equal(idx[sel].cpu().numpy(), ridx)
+    assert_close_layer(bf16_to_f64(out[sel]), ref)
