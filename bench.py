@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""bench.py -- MoE-layer tokens/s and max-GPU p99 latency on B200, balanced vs
+contiguous placement (BASELINE.json metric), through libmoe's C ABI.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config mixtral|tiny|e64] [--zipf-s S] [--placement contiguous|balanced|both]
+
+A step is one pass of the whole hot path over one
+batch: moe_route -> moe_route_stats (layer l-1 -> l) -> moe_dispatch ->
+moe_expert_ffn -> moe_combine.  Workload at every N: the Mixtral-8x7B MoE layer
+(E=8, top-2, H=4096, F=14336) over T = 16384 tokens in total (reading G15),
+Zipf-skewed router logits (s = 1.6, the paper's 64% layer-14 skew),
+synthetic bf16 data, random-init weights.  T is split across the N EP ranks
+(strong scaling); N = 1 hosts all 8 experts on one GPU.
+
+Timing: W untimed warm-up steps, then K steps bracketed by a barrier and a
+device synchronize on both sides, CUDA events on the launching stream, max over
+ranks.  Inputs are larger than L2 (2.8 GB of expert weights per layer, 128 MiB
+of activations), so no flush is needed between steps.  Rank 0 prints one JSON
+line.  ``--impl reference`` times the CPU oracle (the reference arm for this
+tier) on bounded samples of the same workload.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MoE-layer tokens/s and max-GPU p99 latency at 1/2/4/8 B200, balanced vs contiguous"
+CONFIGS = {
+    "mixtral": dict(workload="mixtral-8x7b-moe-layer", E=8, k=2, H=4096, F=14336, T=16384),
+    "tiny": dict(workload="tiny-moe-layer", E=8, k=2, H=64, F=128, T=1024),
+    "e64": dict(workload="e64-top8-moe-layer", E=64, k=8, H=4096, F=2048, T=65536),
+}
+
+
+def blocks(T, G):
+    base, rem = divmod(T, G)
+    out, s0 = [], 0
+    for s in range(G):
+        n = base + (1 if s < rem else 0)
+        out.append((s0, s0 + n))
+        s0 += n
+    return out
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- oracle (CPU) arm
+def oracle_expert_fn(weights64, weights_bf16):
+    from oracle import ffn
+    from oracle import bf16 as obf
+
+    def to64(t):
+        return obf.from_bits(t.contiguous().view(torch.int16).numpy().view(np.uint16))
+
+    cache = {}
+
+    def fn(e, rows):
+        if weights64 is not None:
+            w1, w3, w2 = weights64[e]
+        else:
+            if e not in cache:
+                cache.clear()
+                cache[e] = tuple(to64(m) for m in weights_bf16[e])
+            w1, w3, w2 = cache[e]
+        return ffn.swiglu(rows, w1, w3, w2)[1]
+    return fn
+
+
+def oracle_setup(cfg, seed, s, G, P):
+    """Host copies of the workload for the oracle (generated by synth on the CPU)."""
+    import psutil
+    from oracle import bf16 as obf
+    E, H, F, T = cfg["E"], cfg["H"], cfg["F"], cfg["T"]
+    x = synth.hidden_states(T, H, seed)
+    logits = synth.zipf_logits(T, E, s, seed)
+    wb = [synth.expert_weights(e, H, F, seed) for e in range(E)]
+    need = E * 3 * H * F * 8
+    w64 = None
+    if psutil.virtual_memory().available > 2.5 * need:
+        w64 = [tuple(obf.from_bits(m.contiguous().view(torch.int16).numpy().view(np.uint16)) for m in q) for q in wb]
+    return x, logits, wb, w64
+
+
+def oracle_time(cfg, n_tok, reps, seed, s, G, P, state=None):
+    """Time oracle.layer.layer_ep on `reps` samples of n_tok tokens of the workload."""
+    from oracle import layer as olayer
+    from oracle import bf16 as obf
+    if state is None:
+        state = oracle_setup(cfg, seed, s, G, P)
+    x, logits, wb, w64 = state
+    fn = oracle_expert_fn(w64, wb)
+    rng = np.random.default_rng(seed + 99)
+    times = []
+    for _ in range(reps):
+        sel = np.sort(rng.choice(cfg["T"], n_tok, replace=False))
+        xs = obf.from_bits(x[sel].contiguous().view(torch.int16).numpy().view(np.uint16))
+        ls = logits[sel].numpy()
+        t0 = time.perf_counter()
+        olayer.layer_ep(xs, ls, cfg["k"], np.asarray(P), G, fn)
+        times.append(time.perf_counter() - t0)
+    return times, state
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count()
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    from paper_2502_06643_b200 import moe, placement
+
+    cfg = CONFIGS[args.config]
+    E, k, H, F, T = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["T"]
+    N = args.gpus
+    rank = int(os.environ.get("RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != N:
+        raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}; launch N>1 with torch.distributed.run")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(moe.get_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        uid = bytes(uid.cpu().numpy().tobytes())
+    else:
+        uid = None
+    bl = blocks(T, N)
+    t0, t1 = bl[rank]
+    Tr = t1 - t0
+    Tmax = max(b - a for a, b in bl)
+    lay = moe.MoeLayer(max_tokens=max(Tmax, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N, rank=rank,
+                       device=local, uid=uid)
+    s = args.zipf_s
+    x = synth.hidden_states(T, H, args.seed, device=dev)[t0:t1].contiguous()
+    logits = synth.zipf_logits(T, E, s, args.seed, device=dev)[t0:t1].contiguous()
+    logits_prev = synth.zipf_logits(T, E, s, args.seed + 1, device=dev)[t0:t1].contiguous()
+    idx_prev, _ = lay.route(logits_prev, k)
+    idx = torch.empty(Tr, k, dtype=torch.int32, device=dev)
+    wts = torch.empty(Tr, k, dtype=torch.float32, device=dev)
+    out = torch.empty(Tr, H, dtype=torch.bfloat16, device=dev)
+    load = torch.zeros(E, dtype=torch.int64, device=dev)
+    coact = torch.zeros(E, E, dtype=torch.int64, device=dev)
+
+    # placements: Megatron contiguous and MoETuner ILP-1 balanced from the
+    # GPU's own routing statistics (profile -> ILP -> placement)
+    placements = {}
+    if args.placement in ("contiguous", "both"):
+        placements["contiguous"] = moe.placement_contiguous(E, N)
+    if args.placement in ("balanced", "both") and (N > 1 or args.placement == "balanced"):
+        prof_load = torch.zeros(E, dtype=torch.int64, device=dev)
+        pidx, _ = lay.route(logits, k)
+        lay.route_stats(pidx, None, prof_load, None)
+        lay.stats_allreduce(prof_load, None)
+        lay.sync()
+        placements["balanced"] = placement.balanced(prof_load.cpu().numpy(), N).astype(np.int32)
+
+    weights = {}
+    for name, P in placements.items():
+        hosted = [e for e in range(E) if P[e] == rank]
+        if not hosted:
+            weights[name] = (None, None)
+            continue
+        ws = [synth.expert_weights(e, H, F, args.seed, device=dev) for e in hosted]
+        w1 = torch.stack([q[0] for q in ws])
+        w3 = torch.stack([q[1] for q in ws])
+        w2 = torch.stack([q[2] for q in ws])
+        del ws
+        w13 = moe.pack_w13(w1, w3)
+        del w1, w3
+        weights[name] = (w13, w2)
+    torch.cuda.synchronize()
+
+    def step(P, w13, w2):
+        lay.route(logits, k, idx, wts)
+        lay.route_stats(idx_prev, idx, load, coact)
+        lay.dispatch(x, idx, P)
+        if w13 is not None:
+            lay.expert_ffn(w13, w2)
+        lay.combine(wts, out)
+
+    def barrier():
+        if N > 1:
+            dist.barrier()
+
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if N > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.cpu().numpy()
+
+    def mean_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if N > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            t /= N
+        return t.cpu().numpy()
+
+    stream = torch.cuda.current_stream()
+    results = {}
+    peaks, peaks_src = measured_peaks()
+    for name, P in placements.items():
+        w13, w2 = weights[name]
+        info = lay.dispatch(x, idx_prev, P, info=True)  # layout of a representative routing (untimed)
+        for _ in range(args.warmup):
+            step(P, w13, w2)
+        lay.ffn_timing(args.steps)
+        clocks = ClockSampler(local) if rank == 0 else None
+        barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+            time.sleep(0.25)
+        launches0 = lay.kernel_launches
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        barrier()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for i in range(args.steps):
+            step(P, w13, w2)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        launches = lay.kernel_launches - launches0
+        clk = clocks.stop() if clocks else None
+        per_step = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+        total = ev[0].elapsed_time(ev[-1])
+        ffn_ms = lay.ffn_timing_read()
+        k5 = [a for a, b in ffn_ms]
+        k6 = [b for a, b in ffn_ms]
+        per_step_max = max_over_ranks(per_step)
+        per_step_mean = mean_over_ranks(per_step)
+        total_max = float(max_over_ranks([total])[0])
+        rows_here = int(info.recv_rows) if info is not None else 0
+        recv_counts = list(info.recv_counts)[:N]
+        res = dict(
+            total_ms=total_max, ms_per_step=total_max / args.steps,
+            p50_ms=float(np.percentile(per_step_max, 50)), p99_ms=float(np.percentile(per_step_max, 99)),
+            mean_of_max_ms=float(np.mean(per_step_max)), mean_over_ranks_ms=float(np.mean(per_step_mean)),
+            tokens_per_s=T / (total_max / args.steps / 1e3), expert_to_rank=[int(v) for v in P],
+            recv_rows_per_rank=recv_counts, clocks=clk, launches=launches,
+            k5_ms=float(np.mean(k5)) if k5 else None, k6_ms=float(np.mean(k6)) if k6 else None,
+            rows_rank0=rows_here)
+        results[name] = res
+
+    # ---- end-to-end through the public API with host buffers (headline placement)
+    head = "contiguous" if "contiguous" in placements else next(iter(placements))
+    P = placements[head]
+    w13, w2 = weights[head]
+    x_h = x.cpu().pin_memory()
+    l_h = logits.cpu().pin_memory()
+    o_h = torch.empty(Tr, H, dtype=torch.bfloat16).pin_memory()
+    e2e_steps = max(3, args.steps // 2)
+    for _ in range(2):
+        x.copy_(x_h, non_blocking=True)
+        logits.copy_(l_h, non_blocking=True)
+        step(P, w13, w2)
+        o_h.copy_(out, non_blocking=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        x.copy_(x_h, non_blocking=True)
+        logits.copy_(l_h, non_blocking=True)
+        step(P, w13, w2)
+        o_h.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = float(max_over_ranks([e0.elapsed_time(e1) / e2e_steps])[0])
+    h2d = (x.numel() * 2 + logits.numel() * 4) * N
+    d2h = out.numel() * 2 * N
+
+    if rank == 0:
+        r = results[head]
+        R = r["rows_rank0"]
+        flops_k5 = 4.0 * H * F * R
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        ach = flops_k5 / (r["k5_ms"] * 1e-3) / 1e12 if r["k5_ms"] else None
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            traffic = tj.get(f"{args.config}_N{N}_{head}", {}).get("k5_dram_bytes")
+        line = {
+            "metric": METRIC, "value": r["tokens_per_s"], "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded Zipf logits, N(0,1) tokens, random-init weights)",
+            "config": {"workload": cfg["workload"], "experts": E, "top_k": k, "hidden": H, "ffn": F,
+                       "tokens_total": T, "ep": N, "placement": head, "zipf_s": s, "seed": args.seed,
+                       "l2": "no flush: inputs larger than L2 (expert weights 2.8 GB, activations 128 MiB)"
+                       if args.config == "mixtral" else "no flush"},
+            "p50_ms": r["p50_ms"], "p99_ms": r["p99_ms"], "mean_over_ranks_ms": r["mean_over_ranks_ms"],
+            "e2e": {"value": T / (e2e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": r["launches"],
+            "roofline": {"kernel": "K5 grouped GEMM gate/up + fused SwiGLU (tcgen05)", "bound": "tensor",
+                         "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (ach / peak) if ach else None, "traffic": traffic,
+                         "flops_per_launch": flops_k5, "launch_ms": r["k5_ms"],
+                         "peak_source": peaks_src + " bf16 sustained (kernel timed inside a long step)",
+                         "frac_of_burst": (ach / peaks.get("bf16_tflops")) if ach else None,
+                         "k6_ms": r["k6_ms"],
+                         "k6_frac": (2.0 * H * F * R / (r["k6_ms"] * 1e-3) / 1e12 / peak) if r["k6_ms"] else None},
+            "clocks": r["clocks"],
+            "placements": {n: {kk: v for kk, v in res.items() if kk not in ("clocks",)} for n, res in results.items()},
+        }
+        if N == 1 and not args.no_cpu_baseline:
+            times, _ = oracle_time(cfg, args.cpu_tokens, args.cpu_reps, args.seed, s, 1, np.zeros(E, np.int32))
+            line["cpu_baseline"] = {
+                "value": args.cpu_tokens * len(times) / sum(times), "unit": "tokens/s", "cores": threads_used(),
+                "kind": "oracle",
+                "sample": f"{args.cpu_reps} x {args.cpu_tokens} random tokens of the same workload through "
+                          f"oracle.layer.layer_ep (float64 numpy, G=1); weights pre-converted bf16->float64 "
+                          f"outside the timed region; total {sum(times):.1f} s"}
+        print(json.dumps(line), flush=True)
+    if N > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    lay.close()
+
+
+def run_reference(args):
+    """Reference arm for this tier: the CPU oracle, as it stands, on bounded samples."""
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    N = args.gpus
+    E = cfg["E"]
+    P = np.array([e // (E // N) for e in range(E)], dtype=np.int32) if E % N == 0 else np.zeros(E, np.int32)
+    G = N if E % N == 0 else 1
+    state = oracle_setup(cfg, args.seed, args.zipf_s, G, P)
+    if args.warmup:
+        oracle_time(cfg, args.ref_tokens, min(args.warmup, 3), args.seed, args.zipf_s, G, P, state)
+    times, _ = oracle_time(cfg, args.ref_tokens, args.steps, args.seed + 1, args.zipf_s, G, P, state)
+    total = sum(times)
+    val = args.ref_tokens * len(times) / total
+    ms = total / len(times) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": N,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "experts": E, "top_k": cfg["k"], "hidden": cfg["H"],
+                       "ffn": cfg["F"], "tokens_total": cfg["T"], "ep": G, "placement": "contiguous",
+                       "zipf_s": args.zipf_s},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads_used(), "kind": "oracle",
+                             "sample": f"each step = {args.ref_tokens} random tokens of the workload through "
+                                       f"oracle.layer.layer_ep (float64 numpy) on the host cores"},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    del world
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=list(CONFIGS), default="mixtral")
+    ap.add_argument("--zipf-s", type=float, default=1.6)
+    ap.add_argument("--placement", choices=["contiguous", "balanced", "both"], default="both")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=128)
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--ref-tokens", type=int, default=32)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        raise SystemExit("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -200,12 +200,15 @@ moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, 
  * gpu_launches count). */
 int64_t moe_kernel_launches(moe_ctx_t ctx);
 
-/* Per-kernel timing of moe_expert_ffn: when enabled, CUDA events are recorded
- * on the call's stream around the K5 (gate/up + SwiGLU) and K6 (down) GEMM
- * launches.  moe_ffn_timing_read synchronises on those events and writes the
- * last call's durations in milliseconds: ms[0] = K5, ms[1] = K6 (host). */
-moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t enable);
-moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms);
+/* Per-kernel timing of moe_expert_ffn.  moe_ffn_timing_enable(ctx, n) arms n
+ * records (0 disarms): each of the next n moe_expert_ffn calls records CUDA
+ * events on its stream around the K5 (gate/up + SwiGLU) and K6 (down) GEMM
+ * launches -- no host synchronisation.  moe_ffn_timing_read synchronises on
+ * the recorded events, writes ms[i][0] = K5 and ms[i][1] = K6 durations in
+ * milliseconds for every record i < *n_out (host float [max_records][2]) and
+ * re-arms the records. */
+moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t max_records);
+moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms, int32_t max_records, int32_t* n_out);
 
 #ifdef __cplusplus
 }

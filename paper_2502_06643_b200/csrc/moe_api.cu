@@ -59,9 +59,9 @@ struct moe_ctx {
   const void* tmB2_ptr = nullptr;
   int tmB_nw = -1;
 
-  // optional K5/K6 timing events
-  bool timing = false;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // optional K5/K6 timing event records (3 events per moe_expert_ffn call)
+  std::vector<cudaEvent_t> ev;
+  int timing_used = 0;
 
   // last dispatch
   bool have_plan = false;
@@ -535,33 +535,44 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     ctx->tmB2_ptr = w2;
     ctx->tmB_nw = nw_rows;
   }
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[0], s));
+  const bool rec = ctx->timing_used < (int)ctx->ev.size() / 3;
+  cudaEvent_t* ev = rec ? &ctx->ev[3 * ctx->timing_used] : nullptr;
+  if (rec) CU(cudaEventRecord(ev[0], s));
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
                                       ctx->num_sms, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[1], s));
+  if (rec) CU(cudaEventRecord(ev[1], s));
   e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
-  if (ctx->timing) CU(cudaEventRecord(ctx->ev[2], s));
+  if (rec) {
+    CU(cudaEventRecord(ev[2], s));
+    ++ctx->timing_used;
+  }
   ctx->launches += 2;
   return MOE_OK;
 }
 
-moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t enable) {
-  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t max_records) {
+  if (!ctx || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   CU(cudaSetDevice(ctx->cfg.device));
-  for (auto& e : ctx->ev)
-    if (!e) CU(cudaEventCreate(&e));
-  ctx->timing = enable != 0;
+  CU(cudaDeviceSynchronize());
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  ctx->ev.assign((size_t)3 * max_records, nullptr);
+  for (auto& e : ctx->ev) CU(cudaEventCreate(&e));
+  ctx->timing_used = 0;
   return MOE_OK;
 }
 
-moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms) {
-  if (!ctx || !ms) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
-  if (!ctx->ev[2]) return fail(ctx, MOE_ERR_INVALID_ARG, "timing was never enabled");
-  CU(cudaEventSynchronize(ctx->ev[2]));
-  CU(cudaEventElapsedTime(&ms[0], ctx->ev[0], ctx->ev[1]));
-  CU(cudaEventElapsedTime(&ms[1], ctx->ev[1], ctx->ev[2]));
+moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms, int32_t max_records, int32_t* n_out) {
+  if (!ctx || !ms || !n_out || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  const int n = std::min(ctx->timing_used, max_records);
+  for (int i = 0; i < n; ++i) {
+    CU(cudaEventSynchronize(ctx->ev[3 * i + 2]));
+    CU(cudaEventElapsedTime(&ms[2 * i], ctx->ev[3 * i], ctx->ev[3 * i + 1]));
+    CU(cudaEventElapsedTime(&ms[2 * i + 1], ctx->ev[3 * i + 1], ctx->ev[3 * i + 2]));
+  }
+  *n_out = n;
+  ctx->timing_used = 0;
   return MOE_OK;
 }
 

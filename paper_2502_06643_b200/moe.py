@@ -69,7 +69,7 @@ def load_library(path=LIB_PATH):
         "moe_debug_identity_ffn": [P, P],
         "moe_debug_recv": [P, P, I64, P],
         "moe_ffn_timing_enable": [P, I32],
-        "moe_ffn_timing_read": [P, P],
+        "moe_ffn_timing_read": [P, P, I32, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -182,13 +182,18 @@ class MoeLayer:
     def kernel_launches(self):
         return int(_lib.moe_kernel_launches(self._ctx))
 
-    def ffn_timing(self, enable=True):
-        self._c(_lib.moe_ffn_timing_enable(self._ctx, 1 if enable else 0))
+    def ffn_timing(self, max_records):
+        """Arm per-call K5/K6 event records for the next max_records expert_ffn calls."""
+        self._c(_lib.moe_ffn_timing_enable(self._ctx, int(max_records)))
+        self._timing_max = int(max_records)
 
     def ffn_timing_read(self):
-        ms = (ctypes.c_float * 2)()
-        self._c(_lib.moe_ffn_timing_read(self._ctx, ms))
-        return float(ms[0]), float(ms[1])
+        """[(k5_ms, k6_ms)] of the recorded calls (synchronises; re-arms)."""
+        n = getattr(self, "_timing_max", 0)
+        ms = (ctypes.c_float * (2 * max(n, 1)))()
+        got = ctypes.c_int32()
+        self._c(_lib.moe_ffn_timing_read(self._ctx, ms, n, ctypes.byref(got)))
+        return [(float(ms[2 * i]), float(ms[2 * i + 1])) for i in range(got.value)]
 
     def sync(self):
         self._c(_lib.moe_ctx_sync(self._ctx))
