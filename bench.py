@@ -254,13 +254,16 @@ def run_ours(args):
         weights[name] = (w13, w2)
     torch.cuda.synchronize()
 
-    def step(P, w13, w2):
-        lay.route(logits, k, idx, wts)
-        lay.route_stats(idx_prev, idx, load, coact)
-        lay.dispatch(x, idx, P)
+    def step(P, w13, w2, xs=None, ls=None, os_=None, st=None):
+        xs = x if xs is None else xs
+        ls = logits if ls is None else ls
+        os_ = out if os_ is None else os_
+        lay.route(ls, k, idx, wts, stream=st)
+        lay.route_stats(idx_prev, idx, load, coact, stream=st)
+        lay.dispatch(xs, idx, P, stream=st)
         if w13 is not None:
-            lay.expert_ffn(w13, w2)
-        lay.combine(wts, out)
+            lay.expert_ffn(w13, w2, stream=st)
+        lay.combine(wts, os_, stream=st)
 
     def barrier():
         if N > 1:
@@ -331,25 +334,51 @@ def run_ours(args):
     head = "contiguous" if "contiguous" in placements else next(iter(placements))
     P = placements[head]
     w13, w2 = weights[head]
-    x_h = x.cpu().pin_memory()
-    l_h = logits.cpu().pin_memory()
-    o_h = torch.empty(Tr, H, dtype=torch.bfloat16).pin_memory()
-    e2e_steps = max(3, args.steps // 2)
-    for _ in range(2):
-        x.copy_(x_h, non_blocking=True)
-        logits.copy_(l_h, non_blocking=True)
-        step(P, w13, w2)
-        o_h.copy_(out, non_blocking=True)
+    # Every step copies its inputs (x, logits) host->device from pinned memory and
+    # its output device->host.  Copies run on their own streams, double-buffered,
+    # so step i+1's upload and step i-1's download overlap step i's compute.
+    x_h = [x.cpu().pin_memory() for _ in range(2)]
+    l_h = [logits.cpu().pin_memory() for _ in range(2)]
+    o_h = [torch.empty(Tr, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    xb = [x, torch.empty_like(x)]
+    lb = [logits, torch.empty_like(logits)]
+    ob = [out, torch.empty_like(out)]
+    s_up, s_down = torch.cuda.Stream(), torch.cuda.Stream()
+    e2e_steps = max(4, args.steps // 2)
+
+    def e2e_run(n):
+        ev_up = [torch.cuda.Event() for _ in range(n)]
+        ev_comp = [torch.cuda.Event() for _ in range(n)]
+        ev_down = [torch.cuda.Event() for _ in range(n)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(s_up)
+        for i in range(n):
+            b = i % 2
+            with torch.cuda.stream(s_up):
+                if i >= 2:
+                    s_up.wait_event(ev_comp[i - 2])        # slot b no longer read by step i-2
+                xb[b].copy_(x_h[b], non_blocking=True)
+                lb[b].copy_(l_h[b], non_blocking=True)
+                ev_up[i].record(s_up)
+            stream.wait_event(ev_up[i])
+            if i >= 2:
+                stream.wait_event(ev_down[i - 2])          # out slot b downloaded
+            step(P, w13, w2, xb[b], lb[b], ob[b], stream)
+            ev_comp[i].record(stream)
+            with torch.cuda.stream(s_down):
+                s_down.wait_event(ev_comp[i])
+                o_h[b].copy_(ob[b], non_blocking=True)
+                ev_down[i].record(s_down)
+        s_up.wait_event(ev_down[n - 1])
+        if n >= 2:
+            s_up.wait_event(ev_down[n - 2])
+        end.record(s_up)
+        return start, end
+
+    e2e_run(2)
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        x.copy_(x_h, non_blocking=True)
-        logits.copy_(l_h, non_blocking=True)
-        step(P, w13, w2)
-        o_h.copy_(out, non_blocking=True)
-    e1.record(stream)
+    e0, e1 = e2e_run(e2e_steps)
     torch.cuda.synchronize()
     barrier()
     e2e_ms = float(max_over_ranks([e0.elapsed_time(e1) / e2e_steps])[0])
@@ -448,7 +477,7 @@ def main():
     ap.add_argument("--placement", choices=["contiguous", "balanced", "both"], default="both")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=128)
+    ap.add_argument("--cpu-tokens", type=int, default=2048)
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--ref-tokens", type=int, default=32)
     args = ap.parse_args()

@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
 // Per tile: stable in-tile rank of every item among items with the same expert
 // (warp __match_any_sync + per-warp counts), row = base_row + tile_base + rank;
 // then every token row of x is read once (16-byte vectors) and stored k times.
-constexpr int kScatterThreads = 256;
+constexpr int kScatterThreads = 512;
 constexpr int kMaxTileItems = kTileTokens * kMaxK;
 
 struct TileItems {
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
   const int cpr = a.H / 8;
   const int k = a.k;
   const long long total = (long long)(t1 - t0) * cpr;
-  constexpr int U = 4;
+  constexpr int U = 8;
   for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
     uint4 v[U];
 #pragma unroll
@@ -298,6 +298,10 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
 
 // ----------------------------------------------------------------- K8: weighted unpermute
 // out[t] = bf16( sum_{j ascending} w[t][j] * Y[item (t,j)] ), fp32 FMA (reading G4).
+// KT = compile-time k (0: runtime k).  Every (token, 16-byte chunk) pair loads
+// all k source rows before accumulating, so U*k 16-byte loads are in flight per
+// thread; the accumulation order is still j ascending.
+template <int KT>
 __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const float* __restrict__ w, PlanBuffers b,
                                                              const uint4* __restrict__ ybuf,
                                                              const uint4* __restrict__ retbuf,
@@ -307,55 +311,61 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
   __shared__ unsigned char remote_s[kMaxTileItems];
   int s, t0, t1, tile0;
   tile_info(a, blockIdx.x, s, t0, t1, tile0);
-  const int k = a.k;
+  const int k = KT > 0 ? KT : a.k;
   const int n = (t1 - t0) * k;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const long long gi = (long long)t0 * k + i;
     const int v = b.row_of_item[gi];
     row_s[i] = v >= 0 ? v : (v == -1 ? -1 : -(v + 2));
-    w_s[i] = w[gi];
+    w_s[i] = v == -1 ? 0.f : w[gi];
     remote_s[i] = (unsigned char)(v < -1);
   }
   __syncthreads();
   const int cpr = a.H / 8;
   const long long total = (long long)(t1 - t0) * cpr;
-  constexpr int U = 2;
+  constexpr int U = KT == 0 ? 1 : (KT <= 2 ? 4 : (KT <= 4 ? 2 : 1));
+  constexpr int KL = KT == 0 ? 1 : KT;  // rows loaded per batch
   for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
     float acc[U][8];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
-    for (int j = 0; j < k; ++j) {
-      uint4 v[U];
+    for (int j0 = 0; j0 < k; j0 += KL) {
+      uint4 v[U][KL];
+      float wv[U][KL];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long p = p0 + (long long)u * blockDim.x;
-        v[u] = make_uint4(0, 0, 0, 0);
-        if (p < total) {
-          const int tok = (int)(p / cpr), c = (int)(p % cpr);
-          const int i = tok * k + j;
-          const int row = row_s[i];
-          if (row >= 0) v[u] = __ldg((remote_s[i] ? retbuf : ybuf) + (long long)row * cpr + c);
+        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+#pragma unroll
+        for (int jj = 0; jj < KL; ++jj) {
+          v[u][jj] = make_uint4(0, 0, 0, 0);
+          wv[u][jj] = 0.f;
+          if (p < total) {
+            const int i = tok * k + j0 + jj;
+            const int row = row_s[i];
+            if (row >= 0) {
+              v[u][jj] = __ldg((remote_s[i] ? retbuf : ybuf) + (long long)row * cpr + c);
+              wv[u][jj] = w_s[i];
+            }
+          }
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const long long p = p0 + (long long)u * blockDim.x;
-        if (p < total) {
-          const int tok = (int)(p / cpr);
-          const int i = tok * k + j;
-          const float wj = row_s[i] >= 0 ? w_s[i] : 0.f;
-          acc[u][0] = fmaf(wj, bf16_lo(v[u].x), acc[u][0]);
-          acc[u][1] = fmaf(wj, bf16_hi(v[u].x), acc[u][1]);
-          acc[u][2] = fmaf(wj, bf16_lo(v[u].y), acc[u][2]);
-          acc[u][3] = fmaf(wj, bf16_hi(v[u].y), acc[u][3]);
-          acc[u][4] = fmaf(wj, bf16_lo(v[u].z), acc[u][4]);
-          acc[u][5] = fmaf(wj, bf16_hi(v[u].z), acc[u][5]);
-          acc[u][6] = fmaf(wj, bf16_lo(v[u].w), acc[u][6]);
-          acc[u][7] = fmaf(wj, bf16_hi(v[u].w), acc[u][7]);
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int jj = 0; jj < KL; ++jj) {
+          const float wj = wv[u][jj];
+          acc[u][0] = fmaf(wj, bf16_lo(v[u][jj].x), acc[u][0]);
+          acc[u][1] = fmaf(wj, bf16_hi(v[u][jj].x), acc[u][1]);
+          acc[u][2] = fmaf(wj, bf16_lo(v[u][jj].y), acc[u][2]);
+          acc[u][3] = fmaf(wj, bf16_hi(v[u][jj].y), acc[u][3]);
+          acc[u][4] = fmaf(wj, bf16_lo(v[u][jj].z), acc[u][4]);
+          acc[u][5] = fmaf(wj, bf16_hi(v[u][jj].z), acc[u][5]);
+          acc[u][6] = fmaf(wj, bf16_lo(v[u][jj].w), acc[u][6]);
+          acc[u][7] = fmaf(wj, bf16_hi(v[u][jj].w), acc[u][7]);
         }
-      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -411,7 +421,18 @@ void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, co
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, const uint16_t* ybuf,
                     const uint16_t* retbuf, uint16_t* out, cudaStream_t s) {
   if (a.n_tiles > 0)
-    k_combine<<<a.n_tiles, kScatterThreads, 0, s>>>(a, w, b, (const uint4*)ybuf, (const uint4*)retbuf, (uint4*)out);
+  {
+    auto go = [&](auto kern) {
+      kern<<<a.n_tiles, kScatterThreads, 0, s>>>(a, w, b, (const uint4*)ybuf, (const uint4*)retbuf, (uint4*)out);
+    };
+    switch (a.k) {
+      case 1: go(k_combine<1>); break;
+      case 2: go(k_combine<2>); break;
+      case 4: go(k_combine<4>); break;
+      case 8: go(k_combine<8>); break;
+      default: go(k_combine<0>); break;
+    }
+  }
 }
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13, cudaStream_t s) {
   const long long total = (long long)n * 2 * F * (H / 8);

@@ -1,80 +1,94 @@
 // gemm.cu -- K5/K6: persistent grouped bf16 GEMM on tcgen05 tensor cores.
 //
 // Computes, for every hosted expert segment i (rows [row0_i, row0_i + rows_i)
-// of the expert-major receive layout, padded to 128 rows):
+// of the expert-major receive layout, padded to kSegAlign rows):
 //   SWIGLU=true  (K5): acc = A_i W13_i^T (N = 2F, interleaved gate/up blocks of
-//                      BN/2 columns, see moe_pack_w13); D = bf16(silu(g) * u)
+//                      BN/2 rows, see moe_pack_w13); D = bf16(silu(g) * u)
 //   SWIGLU=false (K6): D = bf16(A_i W2_i^T)
 // i.e. the Mixtral SwiGLU expert FFN (reading G5) that the paper runs between
 // the two all-to-alls.  fp32 accumulation in TMEM, fixed K order, no
 // split-K: results are bit-identical for a row regardless of placement or G.
 //
-// Structure (one CTA per SM, persistent, static round-robin tile schedule):
-//   warp 0      TMA producer: A tile [128 x 64] + B tile [BN x 64] per stage,
-//               128-byte swizzle, mbarrier complete_tx
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128, N=BN, K=16 per instruction), tcgen05.commit -> barriers
-//   warps 2..5  epilogue: tcgen05.ld 32x32b (TMEM lane = tile row) -> SwiGLU /
-//               convert -> 16-byte global stores; double-buffered accumulators
-// Tile order: segment, then N tile, then M tile fastest, so the CTAs running
-// concurrently share the same weight tiles (B) and walk the segment's rows (A),
-// which stay resident in the 126 MB L2 across N tiles.
+// Structure: persistent kernel, CG = 2 CTAs per cluster (one per SM of a TPC)
+// cooperating on 256 x BN tiles with tcgen05.mma.cta_group::2 (M = 256), or
+// CG = 1 (M = 128).  Per CTA, 192 threads:
+//   warp 0      TMA producer: its own A half [128 x 64] and B half [BN/CG x 64]
+//               per stage, 128-byte swizzle; completion is signalled on the
+//               leader CTA's mbarrier (cta_group::2 TMA)
+//   warp 1      TMEM allocator (both CTAs) + single-thread MMA issuer (leader
+//               only); tcgen05.commit multicasts stage-free / accumulator-full
+//               to both CTAs
+//   warps 2..5  epilogue: tcgen05.ld 32x32b of this CTA's 128 accumulator
+//               rows -> SwiGLU / convert -> 16-byte global stores; arrive on
+//               the leader's accumulator-empty barrier; double-buffered TMEM
+// Tile order (per segment): groups of kGroupM M tiles; inside a group N tiles
+// outer, M tiles fastest.  Concurrent clusters share weight tiles (B) while the
+// group's activation rows (A, <= 32 MiB) stay resident in the 126 MB L2, so the
+// weights are streamed from HBM once per group instead of A once per N tile.
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace moe {
 
-constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kGemmThreads = 192;
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int kGroupMDefault = 16;  // M tiles per rasterisation group (MOE_GEMM_GROUP_M overrides, for tuning)
 
-template <int BN>
+template <int BN, int CG>
 struct GemmCfg {
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_ROWS = BN / CG;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (kSmemBudget / STAGE_BYTES) > 8 ? 8 : (kSmemBudget / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*seg table*/ + 256 /*barriers*/;
+  static constexpr int TILE_M = 128 * CG;
 };
 
 struct SegSmem {
   int nseg;
   int row0[kMaxExperts];
-  int wrow[kMaxExperts];   // weight index
+  int wrow[kMaxExperts];   // first weight row of the segment's expert
   int mtiles[kMaxExperts];
   int tile0[kMaxExperts + 1];
 };
 
-__device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile, int& arow, int& brow_blk,
-                                            int& ntile) {
+// tile -> (A row of the tile, first weight row of the expert, N tile index)
+__device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile_m, int group_m, int tile, int& arow,
+                                            int& wrow, int& ntile) {
   int i = 0;
-  // segments are few (<= E); linear scan from the last hit would also do
   while (i + 1 < sg.nseg && tile >= sg.tile0[i + 1]) ++i;
   const int local = tile - sg.tile0[i];
   const int mt = sg.mtiles[i];
-  ntile = local / mt;
-  const int mtile = local % mt;
-  arow = sg.row0[i] + mtile * BM;
-  brow_blk = sg.wrow[i];
-  (void)ntn;
+  const int per_group = group_m * ntn;
+  const int g = local / per_group;
+  const int r = local % per_group;
+  const int gm = min(group_m, mt - g * group_m);  // M tiles in this group
+  ntile = r / gm;
+  const int mtile = g * group_m + r % gm;
+  arow = sg.row0[i] + mtile * tile_m;
+  wrow = sg.wrow[i];
 }
 
-template <int BN, bool SWIGLU>
+template <int BN, bool SWIGLU, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K) {
-  using C = GemmCfg<BN>;
+                   uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
+                   int group_m) {
+  using C = GemmCfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + C::STAGES * C::A_BYTES;
-  SegSmem& sg = *reinterpret_cast<SegSmem*>(smem + C::STAGES * C::STAGE_BYTES);
   static_assert(sizeof(SegSmem) <= 8192, "segment table");
+  SegSmem& sg = *reinterpret_cast<SegSmem*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 8192);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
@@ -84,6 +98,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = crank == 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int n_clusters = gridDim.x / CG;
   const int ntn = N / BN;
   const int nkb = K / BK;
 
@@ -94,7 +112,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     for (int i = 0; i < nseg; ++i) {
       const int rows = seg_meta[1 + E + i];
-      const int mt = (rows + BM - 1) / BM;
+      const int mt = (rows + C::TILE_M - 1) / C::TILE_M;
       sg.row0[i] = seg_meta[1 + i];
       sg.wrow[i] = seg_meta[1 + 2 * E + i] * N;
       sg.mtiles[i] = mt;
@@ -112,36 +130,52 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], 4 * CG);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = sg.tile0[sg.nseg];
 
   if (warp == 0) {
     if (lane == 0) {
-      // ================= TMA producer
+      // ================= TMA producer (every CTA loads its halves)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        int arow, bblk, nt;
-        decode_tile(sg, ntn, tile, arow, bblk, nt);
-        const int brow = bblk + nt * BN;
+      for (int tile = cluster_id; tile < total_tiles; tile += n_clusters) {
+        int arow, wrow, nt;
+        decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt);
+        const int a_row = arow + (int)crank * 128;
+        const int b_row = wrow + nt * BN + (int)crank * C::B_ROWS;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(&tmA, &full[stage], smA + stage * C::A_BYTES, kb * BK, arow);
-          tma_load_2d(&tmB, &full[stage], smB + stage * C::B_BYTES, kb * BK, brow);
+          if constexpr (CG == 2) {
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tma_load_2d_pair(&tmA, fb, smA + stage * C::A_BYTES, kb * BK, a_row);
+            tma_load_2d_pair(&tmB, fb, smB + stage * C::B_BYTES, kb * BK, b_row);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(&tmA, &full[stage], smA + stage * C::A_BYTES, kb * BK, a_row);
+            tma_load_2d(&tmB, &full[stage], smB + stage * C::B_BYTES, kb * BK, b_row);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -150,14 +184,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ================= MMA issuer (single thread)
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+    if (lane == 0 && leader) {
+      // ================= MMA issuer (single thread of the leader CTA)
+      constexpr uint32_t idesc = umma_idesc_bf16(C::TILE_M, BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int tile = cluster_id; tile < total_tiles; tile += n_clusters) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -168,16 +202,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b_addr = smem_u32(smB + stage * C::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            umma_bf16(d_tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
-                      (kb | kk) != 0);
+            const uint64_t ad = umma_desc_sw128(a_addr + kk * 32), bd = umma_desc_sw128(b_addr + kk * 32);
+            if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2) umma_commit_pair_mc(&empty[stage], 0x3);
+          else umma_commit(&empty[stage]);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (CG == 2) umma_commit_pair_mc(&tfull[acc], 0x3);
+        else umma_commit(&tfull[acc]);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -189,12 +226,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      int arow, bblk, nt;
-      decode_tile(sg, ntn, tile, arow, bblk, nt);
+    const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+    for (int tile = cluster_id; tile < total_tiles; tile += n_clusters) {
+      int arow, wrow, nt;
+      decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const long long grow = arow + q * 32 + lane;
+      const long long grow = arow + (int)crank * 128 + q * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
       if constexpr (SWIGLU) {
         uint16_t* drow = D + grow * ldd + (long long)nt * (BN / 2);
@@ -236,7 +274,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -245,11 +286,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -261,21 +307,40 @@ int gemm_block_n(int N, bool swiglu) {
   return 64;
 }
 
+int gemm_b_box_rows(int N, bool swiglu) { return gemm_block_n(N, swiglu) / kGemmCG; }
+
 template <int BN, bool SWIGLU>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, cudaStream_t s) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, kGemmCG>;
+  auto kern = k_grouped_gemm<BN, SWIGLU, kGemmCG>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_grouped_gemm<BN, SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(tmA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(tmB);
-  k_grouped_gemm<BN, SWIGLU><<<num_sms, kGemmThreads, C::SMEM, s>>>(a, b, D, ldd, seg_meta, E, N, K);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((num_sms / kGemmCG) * kGemmCG);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kGemmCG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int group_m = 0;
+  if (!group_m) {
+    const char* env = getenv("MOE_GEMM_GROUP_M");
+    group_m = env ? atoi(env) : kGroupMDefault;
+    if (group_m < 1) group_m = kGroupMDefault;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,

@@ -50,6 +50,7 @@ void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H
 // K5/K6 grouped GEMM (gemm.cu).
 struct GemmPlan;  // opaque
 int gemm_block_n(int N, bool swiglu);
+int gemm_b_box_rows(int N, bool swiglu);  // TMA box rows of the B (weight) operand per CTA
 int pack_block(int F);
 // Launch the persistent grouped GEMM: D[rows][ldd] for every hosted expert segment.
 // tmA / tmB are CUtensorMap (128 bytes each) built by make_tmap_2d.

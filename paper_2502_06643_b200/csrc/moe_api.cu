@@ -527,7 +527,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const int H = ctx->H, F = ctx->F;
   const int nw_rows = ctx->virt ? ctx->E : nw;
   if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows) {
-    const int bn1 = gemm_block_n(2 * F, true), bn2 = gemm_block_n(H, false);
+    const int bn1 = gemm_b_box_rows(2 * F, true), bn2 = gemm_b_box_rows(H, false);
     if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)nw_rows * 2 * F, H, bn1) ||
         !make_tmap_2d(ctx->tmB2, w2, (uint64_t)nw_rows * H, F, bn2))
       return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weights");

@@ -1,0 +1,114 @@
+"""Worker for tests/test_multigpu.py (launched with torch.distributed.run, one
+process per GPU).  Runs the EP layer over real ranks with NCCL and checks, on
+every rank:
+  * the plan (dest rank, receive position, send slot, count matrix) is
+    bit-exact with the oracle's C3 plan for this source rank;
+  * the received payload is bit-identical to the oracle's receive order;
+  * the identity-expert round trip returns x bit-exactly;
+  * the layer output equals the single-GPU virtual-rank run bit-exactly
+    (cross-mode equality) and is within tolerance of the oracle.
+Prints "RANK <r> OK" on success.
+"""
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle import layer as olayer  # noqa: E402
+from oracle import plan as oplan  # noqa: E402
+from oracle import route as oroute  # noqa: E402
+from tests._util import Inputs, assert_close_layer, bf16_to_f64  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    from paper_2502_06643_b200 import moe
+
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(moe.get_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    uid = bytes(uid.cpu().numpy().tobytes())
+
+    T, H, F, E, k = 1500, 256, 512, 8, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=21)
+    blocks = oplan.token_blocks(T, world)
+    a, b = blocks[rank]
+    Tmax = max(y - x for x, y in blocks)
+    lay = moe.MoeLayer(max_tokens=Tmax, hidden=H, ffn=F, num_experts=E, max_k=k, world=world, rank=rank,
+                       device=local, uid=uid)
+    ridx, _ = oroute.route(inp.logits.numpy(), k)
+    placements = [np.array([e * world // E for e in range(E)])]
+    bal = np.array([0, 1, 2, 2, 3, 2, 3, 3]) % world
+    placements.append(bal)
+    if world >= 2:
+        placements.append(np.array([world - 1] * 6 + [0, 0]))      # ranks 1..w-2 host nothing
+    x_all, logits_all = inp.to_device(dev)
+    x = x_all[a:b].contiguous()
+    logits = logits_all[a:b].contiguous()
+    virt_out = None
+    for P in placements:
+        idx, w = lay.route(logits, k)
+        lay.dispatch(x, idx, P)
+        dr, rp, ss, cnt = lay.debug_plan()
+        pl = oplan.plan([ridx[x0:y0] for x0, y0 in blocks], P, world)
+        assert np.array_equal(cnt, pl["cnt"]), "count matrix"
+        assert np.array_equal(ss, pl["slot"][rank]), "send slots"
+        assert np.array_equal(rp, pl["recv_pos"][rank]), "receive positions"
+        assert np.array_equal(dr, P[ridx[a:b]]), "destination ranks"
+        rows = lay.debug_recv()
+        xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+        ref_rows = xb[[blocks[s][0] + t for (s, t, j, e) in pl["recv"][rank]]].reshape(-1, H)
+        assert np.array_equal(rows, ref_rows), "received payload"
+        lay.identity_ffn()
+        out = lay.combine(w)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), x.view(torch.int16)), "identity round trip"
+        # real expert FFN
+        hosted = [e for e in range(E) if P[e] == rank]
+        lay.dispatch(x, idx, P)
+        if hosted:
+            w1, w3, w2 = inp.device_weights(dev, hosted)
+            lay.expert_ffn(moe.pack_w13(w1, w3), w2)
+        out = lay.combine(w)
+        lay.sync()
+        if virt_out is None:
+            # single-GPU virtual-rank run of the same layer (all tokens), for cross-mode equality
+            vl = moe.MoeLayer(max_tokens=T, hidden=H, ffn=F, num_experts=E, max_k=k, virtual_ranks=world,
+                              device=local)
+            vi, vw = vl.route(logits_all, k)
+            vl.dispatch(x_all, vi, P)
+            w1, w3, w2 = inp.device_weights(dev, list(range(E)))
+            vl.expert_ffn(moe.pack_w13(w1, w3), w2)
+            virt_out = vl.combine(vw)
+            vl.sync()
+            vl.close()
+            ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+        assert torch.equal(out.view(torch.int16), virt_out[a:b].view(torch.int16)), "cross-mode equality"
+        assert_close_layer(bf16_to_f64(out), ref[a:b])
+    # statistics all-reduce: sum of per-rank loads equals the global load
+    load = torch.zeros(E, dtype=torch.int64, device=dev)
+    idx, _ = lay.route(logits, k)
+    lay.route_stats(idx, None, load, None)
+    lay.stats_allreduce(load, None)
+    lay.sync()
+    assert np.array_equal(load.cpu().numpy(), np.bincount(ridx.ravel(), minlength=E))
+    lay.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"RANK {rank} OK", flush=True)
+
+
+if __name__ == "__main__":
+    main()
