@@ -30,6 +30,8 @@ import sys
 import threading
 import time
 
+os.environ.setdefault("NCCL_DEBUG", "WARN")   # keep rank 0's stdout to the one JSON line
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -213,7 +215,7 @@ def run_ours(args):
     Tr = t1 - t0
     Tmax = max(b - a for a, b in bl)
     lay = moe.MoeLayer(max_tokens=max(Tmax, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N, rank=rank,
-                       device=local, uid=uid)
+                       device=local, uid=uid, a2a=args.a2a)
     s = args.zipf_s
     x = synth.hidden_states(T, H, args.seed, device=dev)[t0:t1].contiguous()
     logits = synth.zipf_logits(T, E, s, args.seed, device=dev)[t0:t1].contiguous()
@@ -328,7 +330,67 @@ def run_ours(args):
             recv_rows_per_rank=recv_counts, clocks=clk, launches=launches,
             k5_ms=float(np.mean(k5)) if k5 else None, k6_ms=float(np.mean(k6)) if k6 else None,
             rows_rank0=rows_here)
+        # per-phase breakdown (separate, untimed-for-value loop): the paper's
+        # "token processing time" (expert FFN) and "all-to-all time" (dispatch +
+        # combine), tail = max over GPUs and average = mean over GPUs
+        nph = 5
+        phase = np.zeros((nph, 5))
+        for i in range(nph):
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            barrier()
+            evs[0].record(stream)
+            lay.route(logits, k, idx, wts)
+            evs[1].record(stream)
+            lay.route_stats(idx_prev, idx, load, coact)
+            evs[2].record(stream)
+            lay.dispatch(x, idx, P)
+            evs[3].record(stream)
+            if w13 is not None:
+                lay.expert_ffn(w13, w2)
+            evs[4].record(stream)
+            lay.combine(wts, out)
+            evs[5].record(stream)
+            torch.cuda.synchronize()
+            phase[i] = [evs[j].elapsed_time(evs[j + 1]) for j in range(5)]
+        pm = phase.mean(0)
+        tail = max_over_ranks(list(pm))
+        avg = mean_over_ranks(list(pm))
+        names = ["route", "route_stats", "dispatch", "expert_ffn", "combine"]
+        res["phases_ms"] = {"tail": dict(zip(names, map(float, tail))), "avg": dict(zip(names, map(float, avg)))}
+        res["paper_metrics_ms"] = {
+            "token_processing_tail": float(tail[3]), "token_processing_avg": float(avg[3]),
+            "all_to_all_tail": float(max_over_ranks([pm[2] + pm[4]])[0]),
+            "all_to_all_avg": float(mean_over_ranks([pm[2] + pm[4]])[0])}
         results[name] = res
+
+    # ---- the 32-layer routing-statistics profiling pass: per layer
+    # moe_route + moe_route_stats(l-1 -> l), then one all-reduce of load/coact
+    L = 32
+    ml = [q[t0:t1].contiguous() for q in synth.multilayer_logits(L, T, E, s, args.seed, device=dev)]
+    idx_l = [torch.empty(Tr, k, dtype=torch.int32, device=dev) for _ in range(L)]
+    w_l = torch.empty(Tr, k, dtype=torch.float32, device=dev)
+    load_l = torch.zeros(L, E, dtype=torch.int64, device=dev)
+    coact_l = torch.zeros(L - 1, E, E, dtype=torch.int64, device=dev)
+
+    def stats_pass_timed():
+        for li in range(L):
+            lay.route(ml[li], k, idx_l[li], w_l)
+            if li:
+                # load of layer l-1 and co-activation l-1 -> l in one pass
+                lay.route_stats(idx_l[li - 1], idx_l[li], load_l[li - 1], coact_l[li - 1])
+        lay.route_stats(idx_l[L - 1], None, load_l[L - 1], None)
+        for li in range(L):
+            lay.stats_allreduce(load_l[li], coact_l[li] if li < L - 1 else None)
+
+    stats_pass_timed()
+    barrier()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    stats_pass_timed()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    stats_ms = float(max_over_ranks([s0.elapsed_time(s1)])[0])
 
     # ---- end-to-end through the public API with host buffers (headline placement)
     head = "contiguous" if "contiguous" in placements else next(iter(placements))
@@ -402,6 +464,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded Zipf logits, N(0,1) tokens, random-init weights)",
             "config": {"workload": cfg["workload"], "experts": E, "top_k": k, "hidden": H, "ffn": F,
                        "tokens_total": T, "ep": N, "placement": head, "zipf_s": s, "seed": args.seed,
+                       "a2a": args.a2a if N > 1 else "none (single GPU)",
                        "l2": "no flush: inputs larger than L2 (expert weights 2.8 GB, activations 128 MiB)"
                        if args.config == "mixtral" else "no flush"},
             "p50_ms": r["p50_ms"], "p99_ms": r["p99_ms"], "mean_over_ranks_ms": r["mean_over_ranks_ms"],
@@ -418,6 +481,9 @@ def run_ours(args):
                          "k6_frac": (2.0 * H * F * R / (r["k6_ms"] * 1e-3) / 1e12 / peak) if r["k6_ms"] else None},
             "clocks": r["clocks"],
             "placements": {n: {kk: v for kk, v in res.items() if kk not in ("clocks",)} for n, res in results.items()},
+            "stats_pass": {"layers": L, "tokens_total": T, "ms": stats_ms, "us_per_layer": stats_ms * 1e3 / L,
+                           "what": "moe_route + moe_route_stats per layer (load and l-1 -> l co-activation), "
+                                   "then moe_stats_allreduce; synth.multilayer_logits (dependency 0.5)"},
         }
         if N == 1 and not args.no_cpu_baseline:
             times, _ = oracle_time(cfg, args.cpu_tokens, args.cpu_reps, args.seed, s, 1, np.zeros(E, np.int32))
@@ -476,6 +542,8 @@ def main():
     ap.add_argument("--zipf-s", type=float, default=1.6)
     ap.add_argument("--placement", choices=["contiguous", "balanced", "both"], default="both")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--a2a", choices=["nccl", "p2p"], default="p2p",
+                    help="all-to-all transport between real ranks (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=2048)
     ap.add_argument("--cpu-reps", type=int, default=2)

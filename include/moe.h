@@ -69,7 +69,15 @@ typedef struct {
   int32_t rank;           /* this process's rank in [0, world) */
   int32_t device;         /* CUDA device ordinal */
   int32_t virtual_ranks;  /* >1 => emulate that many EP ranks (world must be 1) */
-  int32_t a2a_mode;       /* moe_a2a_mode; only MOE_A2A_NCCL is implemented */
+  int32_t a2a_mode;       /* moe_a2a_mode (real ranks only):
+                           * MOE_A2A_NCCL: count all-gather + one host sync to read the
+                           *   G x E count matrix + grouped ncclSend/ncclRecv per (peer, expert);
+                           * MOE_A2A_P2P: receive / expert-output buffers and a signal block
+                           *   are mapped into every peer with CUDA IPC at creation; the
+                           *   count exchange, the dispatch (NVLink stores straight into the
+                           *   hosting rank's receive rows) and the combine (NVLink loads of
+                           *   the hosting rank's output rows) run inside the kernels with
+                           *   epoch-valued release/acquire flags; no host synchronisation. */
 } moe_config;
 
 /* Host-side summary of the last dispatch (optional output of moe_dispatch). */

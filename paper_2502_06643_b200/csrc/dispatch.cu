@@ -1,6 +1,7 @@
 // dispatch.cu -- K2 (placement-aware histogram + stable scan), K3 (16-byte
-// vectorised gather/permute into the receive / send buffers) and K8 (fused
-// weighted unpermute / combine).
+// vectorised gather/permute into the receive / send buffers, or straight into
+// the peer's receive buffer over NVLink), K8 (fused weighted unpermute /
+// combine, pulling peer rows over NVLink in P2P mode), and the P2P flags.
 //
 // Paper: tokens are "routed to remote GPUs using all-to-all communication based
 // on their assigned experts", with the all-to-all before and after
@@ -47,7 +48,33 @@ __device__ __forceinline__ void tile_info(const PlanArgs& a, int tile, int& s, i
     }
     first += nt;
   }
-  s = -1; t0 = t1 = 0; tile0 = first;
+  s = -1;
+  t0 = t1 = 0;
+  tile0 = first;
+}
+
+// ----------------------------------------------------------------- system-scope flags (P2P)
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch) {
+  for (int g = threadIdx.x; g < n; g += blockDim.x)
+    while ((int)(ld_acquire_sys(flags + g) - epoch) < 0) __nanosleep(64);
+  __syncthreads();
+}
+__device__ __forceinline__ unsigned* sig_flag(SigBlock* s, int which, int idx) {
+  return which == 0 ? &s->flag_cnt[idx] : which == 1 ? &s->flag_data[idx] : &s->flag_y[idx];
+}
+// raise flag `which`[me] = epoch on every rank (after making this thread's and,
+// via the caller's barrier, the CTA's prior writes visible system-wide)
+__device__ __forceinline__ void signal_all(const PlanArgs& a, const PlanBuffers& b, int which) {
+  __threadfence_system();
+  for (int g = 0; g < a.G; ++g) st_release_sys(sig_flag(b.peer_sig[g], which, a.me), a.epoch);
 }
 
 // ----------------------------------------------------------------- K2a: per-tile histogram
@@ -124,23 +151,35 @@ __global__ void __launch_bounds__(1024) k_scan(PlanArgs a, PlanBuffers b) {
 }
 
 // ----------------------------------------------------------------- K2c: layout (1 CTA)
-// hosted(e) = virtual mode || P[e] == me.  Hosted experts are ordered by key
-// (P[e], e); each segment is padded to kSegAlign rows.  Writes base_row[s][e]
-// (receive row for hosted e, compact send-buffer row for remote e), the GEMM
-// segment table and totals.
+// In P2P mode the CTA first pushes this rank's count row into every rank's
+// signal block and waits for every source's row (the count all-gather).
+// Per expert e on rank p = P[e]: padded segment start rstart[e] inside rank p's
+// receive buffer (experts ascending), vstart[e] = the same in the concatenated
+// buffer of all ranks (virtual mode).  base_row[s][e] = destination row of the
+// first item of (source s, expert e); NCCL mode sends remote items through a
+// compact send buffer in key (P[e], e) order instead.
 __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers b, long long cap_rows) {
-  __shared__ int rows_s[kMaxExperts], pad_s[kMaxExperts], key_s[kMaxExperts], hosted_s[kMaxExperts];
+  __shared__ int rows_s[kMaxExperts], pad_s[kMaxExperts], p_s[kMaxExperts];
   const int e = threadIdx.x;
   const int E = a.E;
+  const int* cnt = b.cnt_all;
+  if (a.p2p) {
+    if (e < E) {
+      for (int g = 0; g < a.G; ++g) b.peer_sig[g]->cnt[a.me * E + e] = b.cnt_local[e];
+      __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) signal_all(a, b, 0);
+    wait_flags_geq(b.my_sig->flag_cnt, a.G, a.epoch);
+    cnt = b.my_sig->cnt;
+  }
   if (e < E) {
     const int p = b.P[e];
     int r = 0;
-    for (int s = 0; s < a.G; ++s) r += b.cnt_all[s * E + e];
-    const int hosted = a.virt || p == a.me;
+    for (int s = 0; s < a.G; ++s) r += ((volatile const int*)cnt)[s * E + e];
     rows_s[e] = r;
-    pad_s[e] = hosted ? (r + kSegAlign - 1) / kSegAlign * kSegAlign : 0;
-    key_s[e] = p * E + e;
-    hosted_s[e] = hosted;
+    pad_s[e] = (r + kSegAlign - 1) / kSegAlign * kSegAlign;
+    p_s[e] = p;
   }
   __syncthreads();
   int* nseg = b.seg_meta;
@@ -149,31 +188,37 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
   int* seg_w = b.seg_meta + 1 + 2 * E;
   int* totals = b.seg_meta + 1 + 3 * E;  // [0] padded rows, [1] unpadded rows
   if (e < E) {
-    const int my_key = key_s[e];
-    long long start = 0;
-    int pos = 0, send_base = 0;
+    const int p = p_s[e];
+    const int key = p * E + e;
+    long long rstart = 0, vstart = 0;
+    int pos_v = 0, pos_r = 0, send_base = 0;
     for (int q = 0; q < E; ++q) {
-      if (key_s[q] < my_key) {
-        if (hosted_s[q]) {
-          start += pad_s[q];
-          ++pos;
-        } else if (!a.virt) {
-          send_base += b.cnt_all[a.me * E + q];
+      const int kq = p_s[q] * E + q;
+      if (kq < key) {
+        vstart += pad_s[q];
+        ++pos_v;
+        if (p_s[q] == p) {
+          rstart += pad_s[q];
+          ++pos_r;
         }
+        if (!a.virt && !a.p2p && p_s[q] != a.me) send_base += ((volatile const int*)cnt)[a.me * E + q];
       }
     }
-    if (hosted_s[e]) {
+    const bool hosted = a.virt || p == a.me;
+    if (hosted) {
+      const int pos = a.virt ? pos_v : pos_r;
+      const long long start = a.virt ? vstart : rstart;
       seg_row0[pos] = (int)start;
       seg_rows[pos] = rows_s[e];
-      seg_w[pos] = a.virt ? e : pos;
+      seg_w[pos] = a.virt ? e : pos_r;
       if (start + pad_s[e] > cap_rows) atomicOr(b.err, kErrCapacity);
     }
     for (int s = 0; s < a.V; ++s) {
       const int gs = a.virt ? s : a.me;  // global source id of local source s
       int base;
-      if (hosted_s[e]) {
-        long long acc = start;
-        for (int q = 0; q < gs; ++q) acc += b.cnt_all[q * E + e];
+      if (a.virt || a.p2p || hosted) {
+        long long acc = a.virt ? vstart : rstart;
+        for (int q = 0; q < gs; ++q) acc += ((volatile const int*)cnt)[q * E + e];
         base = (int)acc;
       } else {
         base = send_base;
@@ -184,7 +229,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
   if (e == 0) {
     int n = 0, tp = 0, tu = 0;
     for (int q = 0; q < E; ++q)
-      if (hosted_s[q]) {
+      if (a.virt || p_s[q] == a.me) {
         ++n;
         tp += pad_s[q];
         tu += rows_s[q];
@@ -198,14 +243,22 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
 // ----------------------------------------------------------------- K2d + K3: ranks + row copies
 // Per tile: stable in-tile rank of every item among items with the same expert
 // (warp __match_any_sync + per-warp counts), row = base_row + tile_base + rank;
-// then every token row of x is read once (16-byte vectors) and stored k times.
+// then every token row of x is read once (16-byte vectors) and stored k times
+// into the destination chosen by the item's slot: this rank's receive buffer,
+// the compact NCCL send buffer, or (P2P) the receive buffer of rank P[e].
 constexpr int kScatterThreads = 512;
 constexpr int kMaxTileItems = kTileTokens * kMaxK;
 
 struct TileItems {
   int row[kMaxTileItems];
-  unsigned char remote[kMaxTileItems];
+  uint8_t slot[kMaxTileItems];
 };
+
+__device__ __forceinline__ int item_slot(const PlanArgs& a, int p) {
+  if (a.virt) return 0;
+  if (a.p2p) return p;
+  return p == a.me ? 0 : 1;
+}
 
 __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __restrict__ idx, const PlanBuffers& b,
                                            int tile, int s, int t0, int t1, TileItems& it, int* run, int* wcnt) {
@@ -228,21 +281,17 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
     if (e >= 0 && wrank == 0) wcnt[warp * E + e] = __popc(m);
     __syncthreads();
     if (i < n) {
+      int row = -1, slot = 0;
       if (e >= 0) {
         int r = run[e] + wrank;
         for (int w = 0; w < warp; ++w) r += wcnt[w * E + e];
-        const int p = b.P[e];
-        const int remote = !(a.virt || p == a.me);
-        const int row = b.base_row[s * E + e] + b.tile_base[(long long)tile * E + e] + r;
-        it.row[i] = row;
-        it.remote[i] = (unsigned char)remote;
-        // encoding: row >= 0 local (receive buffer), -(row + 2) remote (send/return buffer), -1 invalid
-        b.row_of_item[(long long)t0 * a.k + i] = remote ? -(row + 2) : row;
-      } else {
-        it.row[i] = -1;
-        it.remote[i] = 0;
-        b.row_of_item[(long long)t0 * a.k + i] = -1;
+        row = b.base_row[s * E + e] + b.tile_base[(long long)tile * E + e] + r;
+        slot = item_slot(a, b.P[e]);
       }
+      it.row[i] = row;
+      it.slot[i] = (uint8_t)slot;
+      b.row_of_item[(long long)t0 * a.k + i] = row;
+      b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
     }
     __syncthreads();
     for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
@@ -255,13 +304,16 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
 }
 
 __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const uint4* __restrict__ x,
-                                                             const int32_t* __restrict__ idx, PlanBuffers b,
-                                                             uint4* __restrict__ recv, uint4* __restrict__ sendbuf) {
+                                                             const int32_t* __restrict__ idx, PlanBuffers b) {
   __shared__ TileItems it;
   __shared__ int run[kMaxExperts];
   __shared__ int wcnt[(kScatterThreads / 32) * kMaxExperts];
+  __shared__ uint4* dst_s[kMaxWorld];
+  __shared__ unsigned last;
   int s, t0, t1, tile0;
   tile_info(a, blockIdx.x, s, t0, t1, tile0);
+  const int nslots = a.p2p ? a.G : 2;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) dst_s[q] = b.dst_table[q];
   tile_ranks(a, idx, b, blockIdx.x, s, t0, t1, it, run, wcnt);
   // copy: (token, 16-byte chunk) pairs, consecutive threads -> consecutive chunks
   const int cpr = a.H / 8;
@@ -286,40 +338,55 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
         for (int j = 0; j < k; ++j) {
           const int i = tok * k + j;
           const int row = it.row[i];
-          if (row >= 0) {
-            uint4* dst = it.remote[i] ? sendbuf : recv;
-            dst[(long long)row * cpr + c] = v[u];
-          }
+          if (row >= 0) dst_s[it.slot[i]][(long long)row * cpr + c] = v[u];
         }
       }
     }
   }
+  if (a.p2p) {
+    // the last CTA to finish raises flag_data[me] on every rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(b.done_counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      *b.done_counter = 0;
+      signal_all(a, b, 1);
+    }
+  }
+}
+
+__global__ void k_signal(PlanArgs a, PlanBuffers b, int which) {
+  if (threadIdx.x == 0) signal_all(a, b, which);
 }
 
 // ----------------------------------------------------------------- K8: weighted unpermute
 // out[t] = bf16( sum_{j ascending} w[t][j] * Y[item (t,j)] ), fp32 FMA (reading G4).
 // KT = compile-time k (0: runtime k).  Every (token, 16-byte chunk) pair loads
 // all k source rows before accumulating, so U*k 16-byte loads are in flight per
-// thread; the accumulation order is still j ascending.
+// thread; the accumulation order is still j ascending.  In P2P mode the rows
+// are read from the hosting rank's expert-output buffer over NVLink.
 template <int KT>
 __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const float* __restrict__ w, PlanBuffers b,
-                                                             const uint4* __restrict__ ybuf,
-                                                             const uint4* __restrict__ retbuf,
                                                              uint4* __restrict__ out) {
   __shared__ int row_s[kMaxTileItems];
   __shared__ float w_s[kMaxTileItems];
-  __shared__ unsigned char remote_s[kMaxTileItems];
+  __shared__ uint8_t slot_s[kMaxTileItems];
+  __shared__ const uint4* src_s[kMaxWorld];
   int s, t0, t1, tile0;
   tile_info(a, blockIdx.x, s, t0, t1, tile0);
   const int k = KT > 0 ? KT : a.k;
   const int n = (t1 - t0) * k;
+  const int nslots = a.p2p ? a.G : 2;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = b.src_table[q];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const long long gi = (long long)t0 * k + i;
     const int v = b.row_of_item[gi];
-    row_s[i] = v >= 0 ? v : (v == -1 ? -1 : -(v + 2));
-    w_s[i] = v == -1 ? 0.f : w[gi];
-    remote_s[i] = (unsigned char)(v < -1);
+    row_s[i] = v;
+    w_s[i] = v < 0 ? 0.f : w[gi];
+    slot_s[i] = b.slot_of_item[gi];
   }
+  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, a.epoch);
   __syncthreads();
   const int cpr = a.H / 8;
   const long long total = (long long)(t1 - t0) * cpr;
@@ -346,7 +413,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
             const int i = tok * k + j0 + jj;
             const int row = row_s[i];
             if (row >= 0) {
-              v[u][jj] = __ldg((remote_s[i] ? retbuf : ybuf) + (long long)row * cpr + c);
+              v[u][jj] = __ldg(src_s[slot_s[i]] + (long long)row * cpr + c);
               wv[u][jj] = w_s[i];
             }
           }
@@ -393,7 +460,7 @@ __global__ void k_pack_w13(const uint4* __restrict__ w1, const uint4* __restrict
   for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < total;
        p += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(p % cpr);
-    const long long r2 = p / cpr;            // row in [n*2F]
+    const long long r2 = p / cpr;  // row in [n*2F]
     const int ex = (int)(r2 / (2 * F));
     const int r = (int)(r2 % (2 * F));
     const int blk = r / (2 * B), within = r % (2 * B);
@@ -407,31 +474,30 @@ __global__ void k_pack_w13(const uint4* __restrict__ w1, const uint4* __restrict
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s) {
   if (a.n_tiles > 0) k_count<<<a.n_tiles, 128, 0, s>>>(a, idx, b);
 }
-void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s) {
-  k_scan<<<a.V, 1024, 0, s>>>(a, b);
-}
+void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s) { k_scan<<<a.V, 1024, 0, s>>>(a, b); }
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s) {
   k_layout<<<1, kMaxExperts, 0, s>>>(a, b, (long long)cap_rows);
 }
-void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, uint16_t* recv,
-                    uint16_t* sendbuf, cudaStream_t s) {
-  if (a.n_tiles > 0)
-    k_scatter<<<a.n_tiles, kScatterThreads, 0, s>>>(a, (const uint4*)x, idx, b, (uint4*)recv, (uint4*)sendbuf);
+void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, cudaStream_t s) {
+  if (a.n_tiles > 0) k_scatter<<<a.n_tiles, kScatterThreads, 0, s>>>(a, (const uint4*)x, idx, b);
+  else if (a.p2p) k_signal<<<1, 32, 0, s>>>(a, b, 1);
 }
-void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, const uint16_t* ybuf,
-                    const uint16_t* retbuf, uint16_t* out, cudaStream_t s) {
-  if (a.n_tiles > 0)
-  {
-    auto go = [&](auto kern) {
-      kern<<<a.n_tiles, kScatterThreads, 0, s>>>(a, w, b, (const uint4*)ybuf, (const uint4*)retbuf, (uint4*)out);
-    };
-    switch (a.k) {
-      case 1: go(k_combine<1>); break;
-      case 2: go(k_combine<2>); break;
-      case 4: go(k_combine<4>); break;
-      case 8: go(k_combine<8>); break;
-      default: go(k_combine<0>); break;
-    }
+void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
+  k_signal<<<1, 32, 0, s>>>(a, b, which);
+}
+__global__ void k_wait(const unsigned* flags, int n, unsigned epoch) { wait_flags_geq(flags, n, epoch); }
+void launch_wait(const unsigned* flags, int n, unsigned epoch, cudaStream_t s) {
+  k_wait<<<1, 64, 0, s>>>(flags, n, epoch);
+}
+void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s) {
+  if (a.n_tiles <= 0) return;
+  auto go = [&](auto kern) { kern<<<a.n_tiles, kScatterThreads, 0, s>>>(a, w, b, (uint4*)out); };
+  switch (a.k) {
+    case 1: go(k_combine<1>); break;
+    case 2: go(k_combine<2>); break;
+    case 4: go(k_combine<4>); break;
+    case 8: go(k_combine<8>); break;
+    default: go(k_combine<0>); break;
   }
 }
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13, cudaStream_t s) {

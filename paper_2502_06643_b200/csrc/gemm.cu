@@ -37,7 +37,6 @@ namespace moe {
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kGemmThreads = 192;
 constexpr int kSmemBudget = 200 * 1024;
-constexpr int kGroupMDefault = 16;  // M tiles per rasterisation group (MOE_GEMM_GROUP_M overrides, for tuning)
 
 template <int BN, int CG>
 struct GemmCfg {
@@ -81,8 +80,17 @@ template <int BN, bool SWIGLU, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m) {
+                   int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch) {
   using C = GemmCfg<BN, CG>;
+  // P2P mode: the A rows arrive over NVLink from every source rank; wait for
+  // their arrival flags (system-scope acquire) before any TMA reads them.
+  if (wait_flags != nullptr && threadIdx.x < wait_n) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flags + threadIdx.x) : "memory");
+    } while ((int)(v - epoch) < 0);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy arrivals -> TMA (async proxy)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -311,7 +319,8 @@ int gemm_b_box_rows(int N, bool swiglu) { return gemm_block_n(N, swiglu) / kGemm
 
 template <int BN, bool SWIGLU>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
-                               int N, int K, int num_sms, cudaStream_t s) {
+                               int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
+                               cudaStream_t s) {
   using C = GemmCfg<BN, kGemmCG>;
   auto kern = k_grouped_gemm<BN, SWIGLU, kGemmCG>;
   static bool configured = false;
@@ -334,25 +343,31 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static int group_m = 0;
-  if (!group_m) {
+  // rasterisation group: about 32 MiB of A rows per group (K bytes per row)
+  static int env_group = -1;
+  if (env_group < 0) {
     const char* env = getenv("MOE_GEMM_GROUP_M");
-    group_m = env ? atoi(env) : kGroupMDefault;
-    if (group_m < 1) group_m = kGroupMDefault;
+    env_group = env ? atoi(env) : 0;
   }
-  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m);
+  int group_m = env_group > 0 ? env_group : (int)((32ll << 20) / ((long long)C::TILE_M * K * 2));
+  if (group_m < 1) group_m = 1;
+  if (group_m > 64) group_m = 64;
+  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int num_sms, cudaStream_t s) {
+                                int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags, int wait_n,
+                                unsigned epoch, cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
+#define MOE_GO(BN_, SW_) launch_impl<BN_, SW_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, s)
   if (swiglu) {
-    if (bn == 256) return launch_impl<256, true>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
-    return launch_impl<128, true>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+    if (bn == 256) return MOE_GO(256, true);
+    return MOE_GO(128, true);
   }
-  if (bn == 256) return launch_impl<256, false>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
-  if (bn == 128) return launch_impl<128, false>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
-  return launch_impl<64, false>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, s);
+  if (bn == 256) return MOE_GO(256, false);
+  if (bn == 128) return MOE_GO(128, false);
+  return MOE_GO(64, false);
+#undef MOE_GO
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {

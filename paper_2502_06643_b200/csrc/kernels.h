@@ -10,6 +10,15 @@ void launch_route(const float* logits, int T, int E, int k, int32_t* idx, float*
 void launch_route_stats(const int32_t* idx_l, const int32_t* idx_l1, int T, int E, int k, int64_t* load,
                         int64_t* coact, int* err, int num_sms, cudaStream_t s);
 
+// Shared signal block of one rank (P2P mode), exported to its peers through
+// CUDA IPC.  Peers write their count rows and raise epoch-valued flags here.
+struct SigBlock {
+  int cnt[64 * 256];          // [G][E] count matrix (row s written by source s)
+  unsigned flag_cnt[64];      // flag_cnt[s] = epoch once source s's count row landed
+  unsigned flag_data[64];     // flag_data[s] = epoch once every row s sends here landed
+  unsigned flag_y[64];        // flag_y[g] = epoch once rank g's expert outputs are ready
+};
+
 // Dispatch plan arguments shared by K2/K3/K8 (dispatch.cu).
 struct PlanArgs {
   int T;        // tokens of this process in this call
@@ -20,19 +29,27 @@ struct PlanArgs {
   int G;        // EP group size
   int me;       // real rank (0 in virtual mode)
   int virt;     // 1 = virtual ranks (every expert hosted by this process)
+  int p2p;      // 1 = in-kernel NVLink peer stores/loads (real ranks)
+  unsigned epoch;  // P2P flag value of this dispatch
   int n_tiles;  // sum over sources of ceil(T_s / kTileTokens)
 };
 
-// Device-side plan state (all int32, allocated by the context).
+// Device-side plan state (allocated by the context).
 struct PlanBuffers {
-  const int32_t* P;    // [E] placement
-  int32_t* tile_hist;  // [n_tiles][E]
-  int32_t* tile_base;  // [n_tiles][E]  within-source exclusive prefix
-  int32_t* cnt_local;  // [V][E]
-  const int32_t* cnt_all;  // [G][E]
-  int32_t* base_row;   // [V][E]
-  int32_t* seg_meta;   // [1 + 3E + 4]: nseg, seg_row0[E], seg_rows[E], seg_w[E], totals
-  int32_t* row_of_item;  // [T*k]: row >= 0 local, -(row+2) remote, -1 invalid
+  const int32_t* P;      // [E] placement
+  int32_t* tile_hist;    // [n_tiles][E]
+  int32_t* tile_base;    // [n_tiles][E]  within-source exclusive prefix
+  int32_t* cnt_local;    // [V][E]
+  const int32_t* cnt_all;  // [G][E] (NCCL/virtual); P2P reads SigBlock::cnt of this rank
+  int32_t* base_row;     // [V][E] destination row of the first item of (s, e)
+  int32_t* seg_meta;     // [1 + 3E + 4]: nseg, seg_row0[E], seg_rows[E], seg_w[E], totals
+  int32_t* row_of_item;  // [T*k] destination row (-1: invalid expert id)
+  uint8_t* slot_of_item; // [T*k] index into dst_table / src_table
+  uint4* const* dst_table;        // scatter destinations by slot
+  const uint4* const* src_table;  // combine sources by slot
+  SigBlock* const* peer_sig;      // [G] (P2P) every rank's signal block, own included
+  SigBlock* my_sig;               // (P2P) this rank's signal block
+  unsigned* done_counter;         // last-CTA detection in k_scatter
   int* err;
 };
 
@@ -40,22 +57,25 @@ int plan_tiles(int T, int V);
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
 void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s);
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s);
-void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b,
-                    uint16_t* recv, uint16_t* sendbuf, cudaStream_t s);
-void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, const uint16_t* ybuf,
-                    const uint16_t* retbuf, uint16_t* out, cudaStream_t s);
+void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
+void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s);
+// P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
+void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);
+// P2P: wait until flags[0..n) >= epoch (system-scope acquire).
+void launch_wait(const unsigned* flags, int n, unsigned epoch, cudaStream_t s);
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13,
                      cudaStream_t s);
 
 // K5/K6 grouped GEMM (gemm.cu).
-struct GemmPlan;  // opaque
 int gemm_block_n(int N, bool swiglu);
 int gemm_b_box_rows(int N, bool swiglu);  // TMA box rows of the B (weight) operand per CTA
 int pack_block(int F);
 // Launch the persistent grouped GEMM: D[rows][ldd] for every hosted expert segment.
-// tmA / tmB are CUtensorMap (128 bytes each) built by make_tmap_2d.
+// tmA / tmB are CUtensorMap (128 bytes each) built by make_tmap_2d.  If wait_flags is
+// non-NULL the kernel first waits until wait_flags[0..wait_n) >= epoch (P2P arrivals).
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int num_sms, cudaStream_t s);
+                                int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags,
+                                int wait_n, unsigned epoch, cudaStream_t s);
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 

@@ -63,6 +63,17 @@ struct moe_ctx {
   std::vector<cudaEvent_t> ev;
   int timing_used = 0;
 
+  // per-item destination slot, pointer tables (slot -> buffer), P2P state
+  uint8_t* slot_of_item = nullptr;
+  uint4** dst_table = nullptr;          // device [max(G,2)]
+  const uint4** src_table = nullptr;    // device [max(G,2)]
+  SigBlock** peer_sig = nullptr;        // device [G]
+  SigBlock* sig = nullptr;              // this rank's signal block (IPC-exported)
+  unsigned* done_counter = nullptr;
+  bool p2p = false;
+  unsigned epoch = 0;
+  std::vector<void*> ipc_opened;        // peer mappings to close
+
   // last dispatch
   bool have_plan = false;
   int last_T = 0, last_k = 0, last_tiles = 0;
@@ -106,10 +117,18 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.tile_hist = c->tile_hist;
   b.tile_base = c->tile_base;
   b.cnt_local = c->cnt_local;
-  b.cnt_all = c->virt || c->G == 1 ? c->cnt_local : c->cnt_all;
+  // count matrix [G][E]: the local rows (virtual / G=1), the NCCL all-gather
+  // result, or (P2P) the rows peers wrote into this rank's signal block
+  b.cnt_all = c->virt || c->G == 1 ? c->cnt_local : (c->p2p ? reinterpret_cast<int32_t*>(c->sig) : c->cnt_all);
   b.base_row = c->base_row;
   b.seg_meta = c->seg_meta;
   b.row_of_item = c->row_of_item;
+  b.slot_of_item = c->slot_of_item;
+  b.dst_table = c->dst_table;
+  b.src_table = c->src_table;
+  b.peer_sig = c->peer_sig;
+  b.my_sig = c->sig;
+  b.done_counter = c->done_counter;
   b.err = c->err_dev;
   return b;
 }
@@ -124,6 +143,8 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.G = c->G;
   a.me = c->me;
   a.virt = c->virt;
+  a.p2p = c->p2p;
+  a.epoch = c->epoch;
   a.n_tiles = plan_tiles(T, c->V);
   return a;
 }
@@ -226,7 +247,8 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     return fail(ctx, MOE_ERR_INVALID_ARG, "bad world/rank");
   if (c.virtual_ranks > 1 && c.world != 1) return fail(ctx, MOE_ERR_INVALID_ARG, "virtual_ranks needs world == 1");
   if (c.virtual_ranks > kMaxWorld) return fail(ctx, MOE_ERR_INVALID_ARG, "virtual_ranks > %d", kMaxWorld);
-  if (c.a2a_mode != MOE_A2A_NCCL) return fail(ctx, MOE_ERR_UNSUPPORTED, "only a2a_mode = MOE_A2A_NCCL is implemented");
+  if (c.a2a_mode != MOE_A2A_NCCL && c.a2a_mode != MOE_A2A_P2P)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "unknown a2a_mode %d", c.a2a_mode);
   if (c.world > 1 && !uid) return fail(ctx, MOE_ERR_INVALID_ARG, "uid required when world > 1");
 
   ctx = new moe_ctx();
@@ -286,8 +308,15 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->hbuf, (size_t)ctx->cap_rows * c.ffn * 2) &&
             A((void**)&ctx->ybuf, (size_t)ctx->cap_rows * c.hidden * 2) &&
             A((void**)&ctx->sendbuf, (size_t)ctx->send_rows * c.hidden * 2) &&
-            A((void**)&ctx->retbuf, (size_t)ctx->send_rows * c.hidden * 2);
+            A((void**)&ctx->retbuf, (size_t)ctx->send_rows * c.hidden * 2) &&
+            A((void**)&ctx->slot_of_item, (size_t)std::max<int64_t>(Tm * k, 1)) &&
+            A((void**)&ctx->dst_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
+            A((void**)&ctx->src_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
+            A((void**)&ctx->peer_sig, sizeof(void*) * (size_t)G) &&
+            A((void**)&ctx->sig, sizeof(SigBlock)) && A((void**)&ctx->done_counter, sizeof(unsigned));
   if (!ok) return bail(MOE_ERR_CUDA);
+  cudaMemset(ctx->sig, 0, sizeof(SigBlock));
+  cudaMemset(ctx->done_counter, 0, sizeof(unsigned));
   cudaMemset(ctx->err_dev, 0, sizeof(int));
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
@@ -312,6 +341,66 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       return bail(MOE_ERR_NCCL);
     }
   }
+  // slot -> buffer tables.  NCCL / virtual: slot 0 = this process's receive /
+  // expert-output buffers, slot 1 = the compact send / return buffers.  P2P:
+  // slot g = rank g's receive / expert-output buffer, mapped through CUDA IPC
+  // (NVLink peer memory), exchanged once here over NCCL.
+  {
+    std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr);
+    dst[0] = ctx->recv;
+    dst[1] = ctx->sendbuf;
+    src[0] = ctx->ybuf;
+    src[1] = ctx->retbuf;
+    sig[0] = ctx->sig;
+    if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
+      ctx->p2p = true;
+      cudaIpcMemHandle_t h[3];
+      if (cudaIpcGetMemHandle(&h[0], ctx->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->ybuf) != cudaSuccess ||
+          cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess) {
+        fail(ctx, MOE_ERR_CUDA, "cudaIpcGetMemHandle failed");
+        return bail(MOE_ERR_CUDA);
+      }
+      const size_t hb = sizeof(h);
+      uint8_t* dh = nullptr;
+      std::vector<uint8_t> all(hb * G);
+      if (cudaMalloc(&dh, hb * (G + 1)) != cudaSuccess ||
+          cudaMemcpy(dh + hb * G, h, hb, cudaMemcpyHostToDevice) != cudaSuccess ||
+          ncclAllGather(dh + hb * G, dh, hb, ncclUint8, ctx->comm, 0) != ncclSuccess ||
+          cudaStreamSynchronize(0) != cudaSuccess || cudaMemcpy(all.data(), dh, hb * G, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        if (dh) cudaFree(dh);
+        fail(ctx, MOE_ERR_NCCL, "IPC handle exchange failed");
+        return bail(MOE_ERR_NCCL);
+      }
+      cudaFree(dh);
+      for (int g = 0; g < G; ++g) {
+        if (g == c.rank) {
+          dst[g] = ctx->recv;
+          src[g] = ctx->ybuf;
+          sig[g] = ctx->sig;
+          continue;
+        }
+        const cudaIpcMemHandle_t* hg = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * g);
+        void* p[3] = {nullptr, nullptr, nullptr};
+        for (int i = 0; i < 3; ++i) {
+          cudaError_t e = cudaIpcOpenMemHandle(&p[i], hg[i], cudaIpcMemLazyEnablePeerAccess);
+          if (e != cudaSuccess) {
+            fail(ctx, MOE_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", g, cudaGetErrorString(e));
+            return bail(MOE_ERR_CUDA);
+          }
+          ctx->ipc_opened.push_back(p[i]);
+        }
+        dst[g] = p[0];
+        src[g] = p[1];
+        sig[g] = p[2];
+      }
+    }
+    if (cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->src_table, src.data(), sizeof(void*) * src.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->peer_sig, sig.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+      fail(ctx, MOE_ERR_CUDA, "pointer-table upload failed");
+      return bail(MOE_ERR_CUDA);
+    }
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     fail(ctx, MOE_ERR_CUDA, "device sync after create failed");
     return bail(MOE_ERR_CUDA);
@@ -328,9 +417,11 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
     ncclCommFinalize(ctx->comm);
     ncclCommDestroy(ctx->comm);
   }
+  for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
   void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
-                 ctx->retbuf};
+                 ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
+                 ctx->done_counter};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -441,21 +532,22 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->me);
   ctx->n_hosted = n_hosted;
 
+  if (ctx->p2p) ++ctx->epoch;
   PlanArgs a = plan_args(ctx, T, k);
   PlanBuffers b = plan_buffers(ctx);
   launch_count(a, idx, b, s);
   launch_scan(a, b, s);
   LAUNCHED(ctx, (a.n_tiles > 0) + 1);
-  const bool nccl = ctx->comm != nullptr;
+  const bool nccl = ctx->comm != nullptr && !ctx->p2p;
   if (nccl) {
     NC(ncclAllGather(ctx->cnt_local, ctx->cnt_all, E, ncclInt32, ctx->comm, s));
     CU(cudaMemcpyAsync(ctx->cnt_pinned, ctx->cnt_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     memcpy(ctx->cnt_host.data(), ctx->cnt_pinned, sizeof(int32_t) * G * E);
   }
-  launch_layout(a, b, ctx->cap_rows, s);
-  launch_scatter(a, x, idx, b, ctx->recv, ctx->sendbuf, s);
-  LAUNCHED(ctx, 1 + (a.n_tiles > 0));
+  launch_layout(a, b, ctx->cap_rows, s);  // P2P: also the in-kernel count all-gather
+  launch_scatter(a, x, idx, b, s);        // P2P: NVLink stores into the hosting rank + arrival flags
+  LAUNCHED(ctx, 2);
   if (nccl) {
     const int32_t* P = ctx->P_host.data();
     const int32_t* cnt = ctx->cnt_host.data();
@@ -522,7 +614,15 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   const int nw = ctx->n_hosted;
-  if (nw == 0) return MOE_OK;
+  PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
+  PlanBuffers b = plan_buffers(ctx);
+  if (nw == 0) {
+    if (ctx->p2p) {  // no expert here: still tell every rank "my outputs are ready"
+      launch_signal(a, b, 2, s);
+      LAUNCHED(ctx, 1);
+    }
+    return MOE_OK;
+  }
   if (!w13 || !w2) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL weights");
   const int H = ctx->H, F = ctx->F;
   const int nw_rows = ctx->virt ? ctx->E : nw;
@@ -538,17 +638,24 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const bool rec = ctx->timing_used < (int)ctx->ev.size() / 3;
   cudaEvent_t* ev = rec ? &ctx->ev[3 * ctx->timing_used] : nullptr;
   if (rec) CU(cudaEventRecord(ev[0], s));
+  // P2P: K5 first waits for every source's arrival flag of this dispatch
+  const unsigned* wait = ctx->p2p ? ctx->sig->flag_data : nullptr;
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
-                                      ctx->num_sms, s);
+                                      ctx->num_sms, wait, ctx->G, ctx->epoch, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
-  e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms, s);
+  e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms,
+                          nullptr, 0, 0, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
     ++ctx->timing_used;
   }
   ctx->launches += 2;
+  if (ctx->p2p) {  // expert outputs of this rank are ready for the peers' combine
+    launch_signal(a, b, 2, s);
+    LAUNCHED(ctx, 1);
+  }
   return MOE_OK;
 }
 
@@ -580,7 +687,17 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
+  PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
+  PlanBuffers b = plan_buffers(ctx);
+  if (ctx->p2p) {
+    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, s);
+    LAUNCHED(ctx, 1);
+  }
   CU(cudaMemcpyAsync(ctx->ybuf, ctx->recv, (size_t)ctx->cap_rows * ctx->H * 2, cudaMemcpyDeviceToDevice, s));
+  if (ctx->p2p) {
+    launch_signal(a, b, 2, s);
+    LAUNCHED(ctx, 1);
+  }
   return MOE_OK;
 }
 
@@ -591,7 +708,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   const int E = ctx->E, G = ctx->G, H = ctx->H;
-  if (ctx->comm) {
+  if (ctx->comm && !ctx->p2p) {  // NCCL mode; P2P mode pulls rows inside K8
     const int32_t* P = ctx->P_host.data();
     const int32_t* cnt = ctx->cnt_host.data();
     std::vector<int32_t> recv_base((size_t)G * E);
@@ -620,7 +737,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   }
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
-  launch_combine(a, w, b, ctx->ybuf, ctx->retbuf, out, s);
+  launch_combine(a, w, b, out, s);
   LAUNCHED(ctx, a.n_tiles > 0);
   return MOE_OK;
 }
@@ -635,9 +752,16 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
   if (st != MOE_OK) return st;
   const int E = ctx->E, G = ctx->G, T = ctx->last_T, k = ctx->last_k;
   std::vector<int32_t> cnt((size_t)G * E), rows((size_t)std::max(1, T * k));
-  const int32_t* cnt_dev = (ctx->virt || G == 1) ? ctx->cnt_local : ctx->cnt_all;
+  std::vector<uint8_t> slots((size_t)std::max(1, T * k));
+  const int32_t* cnt_dev = plan_buffers(ctx).cnt_all;
   CU(cudaMemcpy(cnt.data(), cnt_dev, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost));
-  if (T * k) CU(cudaMemcpy(rows.data(), ctx->row_of_item, sizeof(int32_t) * T * k, cudaMemcpyDeviceToHost));
+  if (T * k) {
+    CU(cudaMemcpy(rows.data(), ctx->row_of_item, sizeof(int32_t) * T * k, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(slots.data(), ctx->slot_of_item, (size_t)T * k, cudaMemcpyDeviceToHost));
+  }
+  // P2P: per-rank padded layout of the destination rank
+  std::vector<int32_t> peer_base((size_t)G * E);
+  moe_layout_host(E, G, ctx->P_host.data(), cnt.data(), nullptr, peer_base.data(), nullptr, nullptr);
   if (cnt_out) memcpy(cnt_out, cnt.data(), sizeof(int32_t) * G * E);
   const int32_t* P = ctx->P_host.data();
   // unpadded receive start of (e, s) on rank P[e]; send-order base of (s, e)
@@ -703,17 +827,28 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
       }
     }
     for (int j = 0; j < k; ++j) {
-      const int32_t v = rows[(size_t)t * k + j];
+      const int64_t row = rows[(size_t)t * k + j];
+      const int slot = slots[(size_t)t * k + j];
       int32_t dr = -1, rp = -1, ss = -1;
-      if (v != -1) {
-        const bool remote = v < -1;
-        const int64_t row = remote ? -(int64_t)v - 2 : v;
-        // find the expert whose range contains the row
+      if (row >= 0) {
+        // find the expert whose range (in the buffer the slot names) contains the row
         for (int e = 0; e < E; ++e) {
           const int64_t n = cnt[(size_t)s * E + e];
           if (n == 0) continue;
-          const int64_t b0 = remote ? rbase[e] : pstart[(size_t)s * E + e];
-          if (remote == !(ctx->virt || P[e] == ctx->me) && row >= b0 && row < b0 + n) {
+          bool match;
+          int64_t b0;
+          if (ctx->virt) {
+            match = slot == 0;
+            b0 = pstart[(size_t)s * E + e];
+          } else if (ctx->p2p) {
+            match = P[e] == slot;
+            b0 = peer_base[(size_t)s * E + e];
+          } else {
+            const bool remote = P[e] != ctx->me;
+            match = slot == (remote ? 1 : 0);
+            b0 = remote ? rbase[e] : pstart[(size_t)s * E + e];
+          }
+          if (match && row >= b0 && row < b0 + n) {
             const int64_t rank_within = row - b0;
             dr = P[e];
             rp = (int32_t)(ustart[(size_t)s * E + e] + rank_within);

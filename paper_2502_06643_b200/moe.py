@@ -151,8 +151,10 @@ class MoeLayer:
     """One libmoe context (one EP rank, or G virtual ranks on one GPU)."""
 
     def __init__(self, *, max_tokens, hidden, ffn, num_experts, max_k, world=1, rank=0, device=0,
-                 virtual_ranks=1, uid=None):
-        self.cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, world, rank, device, virtual_ranks, 0)
+                 virtual_ranks=1, uid=None, a2a="nccl"):
+        mode = {"nccl": 0, "p2p": 1}[a2a]
+        self.cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, world, rank, device, virtual_ranks, mode)
+        self.a2a = a2a
         self.E, self.H, self.F = num_experts, hidden, ffn
         self.G = virtual_ranks if virtual_ranks > 1 else world
         self.device = torch.device("cuda", device)

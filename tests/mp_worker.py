@@ -47,7 +47,7 @@ def main():
     a, b = blocks[rank]
     Tmax = max(y - x for x, y in blocks)
     lay = moe.MoeLayer(max_tokens=Tmax, hidden=H, ffn=F, num_experts=E, max_k=k, world=world, rank=rank,
-                       device=local, uid=uid)
+                       device=local, uid=uid, a2a=os.environ.get("MOE_TEST_A2A", "nccl"))
     ridx, _ = oroute.route(inp.logits.numpy(), k)
     placements = [np.array([e * world // E for e in range(E)])]
     bal = np.array([0, 1, 2, 2, 3, 2, 3, 3]) % world

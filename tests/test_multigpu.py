@@ -18,14 +18,16 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
+@pytest.mark.parametrize("a2a", ["nccl", "p2p"])
 @pytest.mark.parametrize("n", [2, 4])
-def test_ep_over_real_ranks(n):
+def test_ep_over_real_ranks(n, a2a):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    port = 29600 + n + os.getpid() % 500
+    port = 29600 + n + (7 if a2a == "p2p" else 0) + os.getpid() % 500
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    env = dict(os.environ, MOE_TEST_A2A=a2a)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     for rank in range(n):
