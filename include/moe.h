@@ -150,7 +150,10 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
  *   h = bf16( silu(X_e W1_e^T) * (X_e W3_e^T) ),  Y_e = bf16( h W2_e^T )
  * with fp32 accumulation on tcgen05 tensor cores.  w13: bf16 packed
  * [n_w][2F][H] (see moe_pack_w13), w2: bf16 [n_w][H][F]; n_w experts in
- * ascending global id: the hosted experts (real mode) or all E (virtual). */
+ * ascending global id: the hosted experts (real mode) or all E (virtual).
+ * Collective in MOE_A2A_P2P mode: every rank calls it after moe_dispatch, also
+ * a rank hosting no expert (w13/w2 may then be NULL) -- it raises the flag the
+ * peers' moe_combine waits for. */
 moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2,
                           moe_stream_t stream);
 

@@ -20,6 +20,14 @@ constexpr int kMaxWorld = 64;
 // Device error word bits (latched; surfaced by moe_ctx_sync as MOE_ERR_DEVICE).
 constexpr int kErrBadExpert = 1;
 constexpr int kErrCapacity = 2;
+constexpr int kErrTimeout = 4;  // a P2P peer flag never arrived
+constexpr unsigned long long kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 

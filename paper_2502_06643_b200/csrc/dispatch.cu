@@ -62,9 +62,20 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch) {
-  for (int g = threadIdx.x; g < n; g += blockDim.x)
-    while ((int)(ld_acquire_sys(flags + g) - epoch) < 0) __nanosleep(64);
+// Spin (system-scope acquire) until flags[0..n) >= epoch.  A peer that never
+// arrives (a rank that skipped a collective call, a dead process) latches
+// kErrTimeout after kFlagTimeoutNs instead of hanging the GPU.
+__device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch, int* err) {
+  for (int g = threadIdx.x; g < n; g += blockDim.x) {
+    const uint64_t t0 = globaltimer_ns();
+    while ((int)(ld_acquire_sys(flags + g) - epoch) < 0) {
+      __nanosleep(64);
+      if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
+        atomicOr(err, kErrTimeout);
+        break;
+      }
+    }
+  }
   __syncthreads();
 }
 __device__ __forceinline__ unsigned* sig_flag(SigBlock* s, int which, int idx) {
@@ -170,7 +181,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
     }
     __syncthreads();
     if (threadIdx.x == 0) signal_all(a, b, 0);
-    wait_flags_geq(b.my_sig->flag_cnt, a.G, a.epoch);
+    wait_flags_geq(b.my_sig->flag_cnt, a.G, a.epoch, b.err);
     cnt = b.my_sig->cnt;
   }
   if (e < E) {
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
     w_s[i] = v < 0 ? 0.f : w[gi];
     slot_s[i] = b.slot_of_item[gi];
   }
-  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, a.epoch);
+  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, a.epoch, b.err);
   __syncthreads();
   const int cpr = a.H / 8;
   const long long total = (long long)(t1 - t0) * cpr;
@@ -485,9 +496,9 @@ void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, co
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
   k_signal<<<1, 32, 0, s>>>(a, b, which);
 }
-__global__ void k_wait(const unsigned* flags, int n, unsigned epoch) { wait_flags_geq(flags, n, epoch); }
-void launch_wait(const unsigned* flags, int n, unsigned epoch, cudaStream_t s) {
-  k_wait<<<1, 64, 0, s>>>(flags, n, epoch);
+__global__ void k_wait(const unsigned* flags, int n, unsigned epoch, int* err) { wait_flags_geq(flags, n, epoch, err); }
+void launch_wait(const unsigned* flags, int n, unsigned epoch, int* err, cudaStream_t s) {
+  k_wait<<<1, 64, 0, s>>>(flags, n, epoch, err);
 }
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s) {
   if (a.n_tiles <= 0) return;

@@ -80,14 +80,19 @@ template <int BN, bool SWIGLU, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch) {
+                   int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch, int* err) {
   using C = GemmCfg<BN, CG>;
   // P2P mode: the A rows arrive over NVLink from every source rank; wait for
   // their arrival flags (system-scope acquire) before any TMA reads them.
   if (wait_flags != nullptr && threadIdx.x < wait_n) {
     unsigned v;
+    const unsigned long long t0 = globaltimer_ns();
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flags + threadIdx.x) : "memory");
+      if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
+        atomicOr(err, kErrTimeout);
+        break;
+      }
     } while ((int)(v - epoch) < 0);
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy arrivals -> TMA (async proxy)
@@ -320,7 +325,7 @@ int gemm_b_box_rows(int N, bool swiglu) { return gemm_block_n(N, swiglu) / kGemm
 template <int BN, bool SWIGLU>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
-                               cudaStream_t s) {
+                               int* err, cudaStream_t s) {
   using C = GemmCfg<BN, kGemmCG>;
   auto kern = k_grouped_gemm<BN, SWIGLU, kGemmCG>;
   static bool configured = false;
@@ -352,14 +357,15 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   int group_m = env_group > 0 ? env_group : (int)((32ll << 20) / ((long long)C::TILE_M * K * 2));
   if (group_m < 1) group_m = 1;
   if (group_m > 64) group_m = 64;
-  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch);
+  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch, err);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags, int wait_n,
-                                unsigned epoch, cudaStream_t s) {
+                                unsigned epoch, int* err, cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
-#define MOE_GO(BN_, SW_) launch_impl<BN_, SW_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, s)
+#define MOE_GO(BN_, SW_) \
+  launch_impl<BN_, SW_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, s)
   if (swiglu) {
     if (bn == 256) return MOE_GO(256, true);
     return MOE_GO(128, true);

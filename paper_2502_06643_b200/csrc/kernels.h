@@ -62,7 +62,7 @@ void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uin
 // P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);
 // P2P: wait until flags[0..n) >= epoch (system-scope acquire).
-void launch_wait(const unsigned* flags, int n, unsigned epoch, cudaStream_t s);
+void launch_wait(const unsigned* flags, int n, unsigned epoch, int* err, cudaStream_t s);
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13,
                      cudaStream_t s);
 
@@ -75,7 +75,7 @@ int pack_block(int F);
 // non-NULL the kernel first waits until wait_flags[0..wait_n) >= epoch (P2P arrivals).
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags,
-                                int wait_n, unsigned epoch, cudaStream_t s);
+                                int wait_n, unsigned epoch, int* err, cudaStream_t s);
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 

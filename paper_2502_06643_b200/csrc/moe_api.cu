@@ -437,8 +437,10 @@ static moe_status check_device_error(moe_ctx_t ctx) {
   CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   if (e) {
     cudaMemset(ctx->err_dev, 0, sizeof(int));
-    return fail(ctx, MOE_ERR_DEVICE, "device error latched:%s%s", (e & kErrBadExpert) ? " expert id out of range" : "",
-                (e & kErrCapacity) ? " receive capacity exceeded" : "");
+    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s",
+                (e & kErrBadExpert) ? " expert id out of range" : "",
+                (e & kErrCapacity) ? " receive capacity exceeded" : "",
+                (e & kErrTimeout) ? " P2P peer flag timeout (a rank skipped a collective call?)" : "");
   }
   return MOE_OK;
 }
@@ -641,11 +643,11 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // P2P: K5 first waits for every source's arrival flag of this dispatch
   const unsigned* wait = ctx->p2p ? ctx->sig->flag_data : nullptr;
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
-                                      ctx->num_sms, wait, ctx->G, ctx->epoch, s);
+                                      ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
   e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms,
-                          nullptr, 0, 0, s);
+                          nullptr, 0, 0, ctx->err_dev, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
@@ -690,7 +692,7 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
   if (ctx->p2p) {
-    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, s);
+    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, ctx->err_dev, s);
     LAUNCHED(ctx, 1);
   }
   CU(cudaMemcpyAsync(ctx->ybuf, ctx->recv, (size_t)ctx->cap_rows * ctx->H * 2, cudaMemcpyDeviceToDevice, s));

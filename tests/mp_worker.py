@@ -81,6 +81,8 @@ def main():
         if hosted:
             w1, w3, w2 = inp.device_weights(dev, hosted)
             lay.expert_ffn(moe.pack_w13(w1, w3), w2)
+        else:
+            lay.expert_ffn(None, None)      # collective: a rank hosting no expert still calls it
         out = lay.combine(w)
         lay.sync()
         if virt_out is None:

@@ -188,6 +188,8 @@ def run_layer(lay, inp, P, G):
     (2000, 512, 1024, 8, 2, 1, [0] * 8),                   # several M/N/K tiles, ragged M tails
     (1500, 256, 192, 6, 3, 2, [1, 0, 1, 1, 0, 1]),           # F % 128 != 0 -> 128-wide SwiGLU tiles
     (700, 128, 256, 16, 4, 4, [e % 4 for e in range(16)]),
+    (600, 128, 128, 64, 8, 8, [e // 8 for e in range(64)]),   # D5 shape family (E64 top-8), 8 virtual ranks
+    (333, 64, 64, 5, 5, 1, [0] * 5),                         # k = E, ragged everything, BN = 64 tiles
 ])
 def test_layer_parity(cuda_ok, T, H, F, E, k, G, P):
     inp = Inputs(T, H, F, E, k, s=1.6, seed=11)

@@ -4,6 +4,7 @@ fewer than 2 GPUs; the host-side multi-rank logic is covered on CPU by
 tests/test_abi_cpu.py::test_two_rank_gloo_count_exchange_and_layout."""
 
 import os
+import signal
 import subprocess
 import sys
 
@@ -27,8 +28,15 @@ def test_ep_over_real_ranks(n, a2a):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MOE_TEST_A2A=a2a)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
-    out = r.stdout + r.stderr
-    assert r.returncode == 0, out[-4000:]
+    # own process group, so a hung rank is killed together with the launcher
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, cwd=ROOT, env=env,
+                         start_new_session=True)
+    try:
+        out, _ = p.communicate(timeout=300)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, _ = p.communicate()
+        pytest.fail("multi-GPU worker timed out:\n" + out[-4000:])
+    assert p.returncode == 0, out[-4000:]
     for rank in range(n):
         assert f"RANK {rank} OK" in out, out[-4000:]
