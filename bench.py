@@ -363,15 +363,16 @@ def run_ours(args):
             "all_to_all_tail": float(max_over_ranks([pm[2] + pm[4]])[0]),
             "all_to_all_avg": float(mean_over_ranks([pm[2] + pm[4]])[0])}
         if N > 1:
-            # NVLink traffic of this rank per phase: remote rows sent / received x 2H bytes
+            # NVLink traffic this rank drives per phase: its remote routed rows x 2H bytes
+            # (dispatch pushes them to the hosting ranks, combine pulls them back)
             sent = sum(int(info.send_counts[g]) for g in range(N) if g != rank)
-            got = int(info.recv_rows) - int(info.send_counts[rank])
-            nv_bytes = max(sent, got) * 2 * H
-            bw = max_over_ranks([nv_bytes / (pm[2] * 1e-3) / 1e9, nv_bytes / (pm[4] * 1e-3) / 1e9])
+            nv_bytes = sent * 2 * H
+            bw = [nv_bytes / (pm[2] * 1e-3) / 1e9, nv_bytes / (pm[4] * 1e-3) / 1e9]
             res["nvlink"] = {"remote_bytes_per_phase_rank0": nv_bytes,
-                             "max_rank_dispatch_GBps": float(bw[0]), "max_rank_combine_GBps": float(bw[1]),
+                             "dispatch_GBps_rank0": float(bw[0]), "combine_GBps_rank0": float(bw[1]),
                              "peak_GBps": 900.0, "measured_peer_copy_GBps": 770.0,
-                             "note": "phase time includes waiting for the slowest peer"}
+                             "note": "per direction; phase times include the count exchange and, for "
+                                     "combine, waiting for the slowest rank's expert FFN"}
         results[name] = res
 
     # ---- the 32-layer routing-statistics profiling pass: per layer
