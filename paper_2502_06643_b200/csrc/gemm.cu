@@ -37,6 +37,7 @@ namespace moe {
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kGemmThreads = 192;
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSchedRing = 8;  // depth of the tile-scheduler ring
 
 template <int BN, int CG>
 struct GemmCfg {
@@ -47,7 +48,8 @@ struct GemmCfg {
   static constexpr int STAGES = (kSmemBudget / STAGE_BYTES) > 8 ? 8 : (kSmemBudget / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*seg table*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*seg table*/ + 512 /*barriers*/;
+  static_assert((2 * STAGES + 4 + 2 * kSchedRing) * 8 + 4 + 4 * kSchedRing <= 512, "barrier area");
   static constexpr int TILE_M = 128 * CG;
 };
 
@@ -66,12 +68,23 @@ __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile
   while (i + 1 < sg.nseg && tile >= sg.tile0[i + 1]) ++i;
   const int local = tile - sg.tile0[i];
   const int mt = sg.mtiles[i];
-  const int per_group = group_m * ntn;
-  const int g = local / per_group;
-  const int r = local % per_group;
-  const int gm = min(group_m, mt - g * group_m);  // M tiles in this group
-  ntile = r / gm;
-  const int mtile = g * group_m + r % gm;
+  int mtile;
+  if (group_m > 0) {  // groups of group_m M tiles, N outer, M fastest (A group L2-resident)
+    const int per_group = group_m * ntn;
+    const int g = local / per_group;
+    const int r = local % per_group;
+    const int gm = min(group_m, mt - g * group_m);  // M tiles in this group
+    ntile = r / gm;
+    mtile = g * group_m + r % gm;
+  } else {            // groups of -group_m N tiles, M outer, N fastest (weight group L2-resident)
+    const int gfull = -group_m;
+    const int per_group = gfull * mt;
+    const int g = local / per_group;
+    const int r = local % per_group;
+    const int gn = min(gfull, ntn - g * gfull);
+    mtile = r / gn;
+    ntile = g * gfull + r % gn;
+  }
   arow = sg.row0[i] + mtile * tile_m;
   wrow = sg.wrow[i];
 }
@@ -80,7 +93,8 @@ template <int BN, bool SWIGLU, int CG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch, int* err) {
+                   int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch, int* err,
+                   unsigned* sched) {
   using C = GemmCfg<BN, CG>;
   // P2P mode: the A rows arrive over NVLink from every source rank; wait for
   // their arrival flags (system-scope acquire) before any TMA reads them.
@@ -107,7 +121,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = bars + 2 * C::STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  uint64_t* sfull = bars + 2 * C::STAGES + 4;           // tile-scheduler ring
+  uint64_t* sempty = sfull + kSchedRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sempty + kSchedRing);
+  int* sched_tile = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -145,6 +162,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4 * CG);
     }
+    // scheduler ring: published by the leader's producer; consumed by the MMA
+    // issuer, every epilogue warp and (pair mode) the peer's producer
+    for (int s = 0; s < kSchedRing; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], CG == 2 ? 10 : 5);
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -167,12 +190,51 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int total_tiles = sg.tile0[sg.nseg];
 
+  // Dynamic tile scheduler: the leader's producer takes the next tile id from a
+  // global counter (atomicAdd) and publishes it through an mbarrier ring to
+  // every role of both CTAs.  Clusters that run ahead simply take more tiles,
+  // so the tiles in flight are always ~one wave of consecutive ids and the
+  // rasterisation group's operands stay L2-resident (a static round-robin
+  // schedule lets clusters drift apart by several waves).
+  auto take_tile = [&](int& seq) -> int {
+    const int slot = seq % kSchedRing;
+    mbar_wait_cluster(&sfull[slot], (uint32_t)((seq / kSchedRing) & 1));
+    const int t = reinterpret_cast<volatile int*>(sched_tile)[slot];
+    ++seq;
+    return t;
+  };
+  auto release_tile = [&](int seq_after) {
+    const int slot = (seq_after - 1) % kSchedRing;
+    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&sempty[slot]), 0));
+    else mbar_arrive(&sempty[slot]);
+  };
+  (void)cluster_id;
+  (void)n_clusters;
+
   if (warp == 0) {
     if (lane == 0) {
       // ================= TMA producer (every CTA loads its halves)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < total_tiles; tile += n_clusters) {
+      int seq = 0;
+      while (true) {
+        int tile;
+        if (leader) {
+          const int slot = seq % kSchedRing;
+          mbar_wait_cluster(&sempty[slot], (uint32_t)(((seq / kSchedRing) & 1) ^ 1));
+          tile = (int)atomicAdd(sched, 1u);
+          sched_tile[slot] = tile;
+          if constexpr (CG == 2) {
+            st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)tile);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[slot]), 1));
+          }
+          mbar_arrive(&sfull[slot]);
+          ++seq;
+        } else {
+          tile = take_tile(seq);
+          release_tile(seq);
+        }
+        if (tile >= total_tiles) break;
         int arow, wrow, nt;
         decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt);
         const int a_row = arow + (int)crank * 128;
@@ -204,7 +266,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < total_tiles; tile += n_clusters) {
+      int seq = 0;
+      while (true) {
+        const int tile = take_tile(seq);
+        release_tile(seq);
+        if (tile >= total_tiles) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -240,7 +306,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
-    for (int tile = cluster_id; tile < total_tiles; tile += n_clusters) {
+    int seq = 0;
+    while (true) {
+      const int tile = take_tile(seq);
+      __syncwarp();
+      if (lane == 0) release_tile(seq);
+      if (tile >= total_tiles) break;
       int arow, wrow, nt;
       decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt);
       mbar_wait(&tfull[acc], acc_phase);
@@ -301,6 +372,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_before();
   if constexpr (CG == 2) cluster_sync();
   else __syncthreads();
+  // the last CTA to leave resets the scheduler counters for the next launch
+  if (threadIdx.x == 0) {
+    if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+      atomicExch(&sched[0], 0u);
+      atomicExch(&sched[1], 0u);
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 2)
@@ -325,7 +403,7 @@ int gemm_b_box_rows(int N, bool swiglu) { return gemm_block_n(N, swiglu) / kGemm
 template <int BN, bool SWIGLU>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
-                               int* err, cudaStream_t s) {
+                               int* err, unsigned* sched, cudaStream_t s) {
   using C = GemmCfg<BN, kGemmCG>;
   auto kern = k_grouped_gemm<BN, SWIGLU, kGemmCG>;
   static bool configured = false;
@@ -349,23 +427,29 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // rasterisation group: about 32 MiB of A rows per group (K bytes per row)
-  static int env_group = -1;
-  if (env_group < 0) {
+  // (MOE_GEMM_GROUP_M overrides for tuning; a negative value -g selects groups
+  // of g N tiles instead)
+  static bool env_read = false;
+  static int env_group = 0;
+  if (!env_read) {
     const char* env = getenv("MOE_GEMM_GROUP_M");
     env_group = env ? atoi(env) : 0;
+    env_read = true;
   }
-  int group_m = env_group > 0 ? env_group : (int)((32ll << 20) / ((long long)C::TILE_M * K * 2));
+  int group_m = (int)((32ll << 20) / ((long long)C::TILE_M * K * 2));
   if (group_m < 1) group_m = 1;
   if (group_m > 64) group_m = 64;
-  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch, err);
+  if (env_group != 0) group_m = env_group;
+  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch, err,
+                            sched);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags, int wait_n,
-                                unsigned epoch, int* err, cudaStream_t s) {
+                                unsigned epoch, int* err, unsigned* sched, cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
 #define MOE_GO(BN_, SW_) \
-  launch_impl<BN_, SW_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, s)
+  launch_impl<BN_, SW_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, s)
   if (swiglu) {
     if (bn == 256) return MOE_GO(256, true);
     return MOE_GO(128, true);

@@ -75,7 +75,9 @@ int pack_block(int F);
 // non-NULL the kernel first waits until wait_flags[0..wait_n) >= epoch (P2P arrivals).
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags,
-                                int wait_n, unsigned epoch, int* err, cudaStream_t s);
+                                int wait_n, unsigned epoch, int* err, unsigned* sched, cudaStream_t s);
+// sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
+// caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
 

@@ -313,10 +313,10 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->dst_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
             A((void**)&ctx->src_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
             A((void**)&ctx->peer_sig, sizeof(void*) * (size_t)G) &&
-            A((void**)&ctx->sig, sizeof(SigBlock)) && A((void**)&ctx->done_counter, sizeof(unsigned));
+            A((void**)&ctx->sig, sizeof(SigBlock)) && A((void**)&ctx->done_counter, 4 * sizeof(unsigned));
   if (!ok) return bail(MOE_ERR_CUDA);
   cudaMemset(ctx->sig, 0, sizeof(SigBlock));
-  cudaMemset(ctx->done_counter, 0, sizeof(unsigned));
+  cudaMemset(ctx->done_counter, 0, 4 * sizeof(unsigned));  // [0] scatter last-CTA, [2..3] GEMM scheduler
   cudaMemset(ctx->err_dev, 0, sizeof(int));
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
@@ -643,11 +643,11 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // P2P: K5 first waits for every source's arrival flag of this dispatch
   const unsigned* wait = ctx->p2p ? ctx->sig->flag_data : nullptr;
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
-                                      ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev, s);
+                                      ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev, ctx->done_counter + 2, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
   e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms,
-                          nullptr, 0, 0, ctx->err_dev, s);
+                          nullptr, 0, 0, ctx->err_dev, ctx->done_counter + 2, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
