@@ -436,7 +436,10 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
     env_group = env ? atoi(env) : 0;
     env_read = true;
   }
-  int group_m = (int)((32ll << 20) / ((long long)C::TILE_M * K * 2));
+  // measured on B200 with the dynamic scheduler (profiles/r1_v5_gemm_group_sweep.txt):
+  // K = 4096 -> 16 M tiles (32 MiB of A), K = 14336 -> 8 M tiles (~58 MiB)
+  const long long target = K <= 8192 ? (32ll << 20) : (64ll << 20);
+  int group_m = (int)(target / ((long long)C::TILE_M * K * 2));
   if (group_m < 1) group_m = 1;
   if (group_m > 64) group_m = 64;
   if (env_group != 0) group_m = env_group;
