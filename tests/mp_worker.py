@@ -106,6 +106,28 @@ def main():
     lay.stats_allreduce(load, None)
     lay.sync()
     assert np.array_equal(load.cpu().numpy(), np.bincount(ridx.ravel(), minlength=E))
+
+    # degenerate split: fewer tokens than ranks, so some ranks own 0 tokens (G7)
+    # but still take part in every collective call; repeated layers reuse the
+    # buffers (P2P epochs advance)
+    Ts = world // 2
+    sb = oplan.token_blocks(Ts, world)
+    a2, b2 = sb[rank]
+    xs = x_all[:Ts][a2:b2].contiguous()
+    ls = logits_all[:Ts][a2:b2].contiguous()
+    P = placements[0]
+    hosted = [e for e in range(E) if P[e] == rank]
+    w1, w3, w2 = inp.device_weights(dev, hosted) if hosted else (None, None, None)
+    w13 = moe.pack_w13(w1, w3) if hosted else None
+    for rep in range(3):
+        idx, w = lay.route(ls, k)
+        lay.dispatch(xs, idx, P)
+        lay.expert_ffn(w13, w2)
+        out = lay.combine(w)
+        lay.sync()
+        assert out.shape == (b2 - a2, H)
+        if b2 > a2:
+            assert torch.equal(out.view(torch.int16), virt_out[a2:b2].view(torch.int16)), "small-T equality"
     lay.close()
     dist.barrier()
     dist.destroy_process_group()
