@@ -272,7 +272,8 @@ __device__ __forceinline__ int item_slot(const PlanArgs& a, int p) {
 }
 
 __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __restrict__ idx, const PlanBuffers& b,
-                                           int tile, int s, int t0, int t1, TileItems& it, int* run, int* wcnt) {
+                                           int tile, int s, int t0, int t1, TileItems& it, int* run, int* wcnt,
+                                           bool write_plan) {
   const int E = a.E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -301,8 +302,10 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
       }
       it.row[i] = row;
       it.slot[i] = (uint8_t)slot;
-      b.row_of_item[(long long)t0 * a.k + i] = row;
-      b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
+      if (write_plan) {
+        b.row_of_item[(long long)t0 * a.k + i] = row;
+        b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
+      }
     }
     __syncthreads();
     for (int e2 = threadIdx.x; e2 < E; e2 += blockDim.x) {
@@ -321,15 +324,22 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
   __shared__ int wcnt[(kScatterThreads / 32) * kMaxExperts];
   __shared__ uint4* dst_s[kMaxWorld];
   __shared__ unsigned last;
+  // col_split CTAs share a token tile; each recomputes the (cheap) in-tile
+  // ranks and copies one slice of the hidden dimension
+  const int part = blockIdx.x % a.col_split;
+  const int tile = blockIdx.x / a.col_split;
   int s, t0, t1, tile0;
-  tile_info(a, blockIdx.x, s, t0, t1, tile0);
+  tile_info(a, tile, s, t0, t1, tile0);
   const int nslots = a.p2p ? a.G : 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) dst_s[q] = b.dst_table[q];
-  tile_ranks(a, idx, b, blockIdx.x, s, t0, t1, it, run, wcnt);
+  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0);
   // copy: (token, 16-byte chunk) pairs, consecutive threads -> consecutive chunks
   const int cpr = a.H / 8;
+  const int cw = (cpr + a.col_split - 1) / a.col_split;
+  const int c_lo = part * cw;
+  const int width = max(0, min(cpr, c_lo + cw) - c_lo);
   const int k = a.k;
-  const long long total = (long long)(t1 - t0) * cpr;
+  const long long total = (long long)(t1 - t0) * width;
   constexpr int U = 8;
   for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
     uint4 v[U];
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
     for (int u = 0; u < U; ++u) {
       const long long p = p0 + (long long)u * blockDim.x;
       if (p < total) {
-        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        const int tok = (int)(p / width), c = c_lo + (int)(p % width);
         v[u] = __ldg(x + (long long)(t0 + tok) * cpr + c);
       }
     }
@@ -345,7 +355,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
     for (int u = 0; u < U; ++u) {
       const long long p = p0 + (long long)u * blockDim.x;
       if (p < total) {
-        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        const int tok = (int)(p / width), c = c_lo + (int)(p % width);
         for (int j = 0; j < k; ++j) {
           const int i = tok * k + j;
           const int row = it.row[i];
@@ -384,8 +394,9 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
   __shared__ float w_s[kMaxTileItems];
   __shared__ uint8_t slot_s[kMaxTileItems];
   __shared__ const uint4* src_s[kMaxWorld];
+  const int part = blockIdx.x % a.col_split;
   int s, t0, t1, tile0;
-  tile_info(a, blockIdx.x, s, t0, t1, tile0);
+  tile_info(a, blockIdx.x / a.col_split, s, t0, t1, tile0);
   const int k = KT > 0 ? KT : a.k;
   const int n = (t1 - t0) * k;
   const int nslots = a.p2p ? a.G : 2;
@@ -400,7 +411,10 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
   if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, a.epoch, b.err);
   __syncthreads();
   const int cpr = a.H / 8;
-  const long long total = (long long)(t1 - t0) * cpr;
+  const int cw = (cpr + a.col_split - 1) / a.col_split;
+  const int c_lo = part * cw;
+  const int width = max(0, min(cpr, c_lo + cw) - c_lo);
+  const long long total = (long long)(t1 - t0) * width;
   constexpr int U = KT == 0 ? 1 : (KT <= 2 ? 4 : (KT <= 4 ? 2 : 1));
   constexpr int KL = KT == 0 ? 1 : KT;  // rows loaded per batch
   for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
@@ -415,7 +429,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long long p = p0 + (long long)u * blockDim.x;
-        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        const int tok = (int)(p / width), c = c_lo + (int)(p % width);
 #pragma unroll
         for (int jj = 0; jj < KL; ++jj) {
           v[u][jj] = make_uint4(0, 0, 0, 0);
@@ -449,7 +463,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
     for (int u = 0; u < U; ++u) {
       const long long p = p0 + (long long)u * blockDim.x;
       if (p < total) {
-        const int tok = (int)(p / cpr), c = (int)(p % cpr);
+        const int tok = (int)(p / width), c = c_lo + (int)(p % width);
         uint4 o;
         o.x = pack_bf16x2(acc[u][0], acc[u][1]);
         o.y = pack_bf16x2(acc[u][2], acc[u][3]);
@@ -490,7 +504,8 @@ void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cu
   k_layout<<<1, kMaxExperts, 0, s>>>(a, b, (long long)cap_rows);
 }
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, cudaStream_t s) {
-  if (a.n_tiles > 0) k_scatter<<<a.n_tiles, kScatterThreads, 0, s>>>(a, (const uint4*)x, idx, b);
+  if (a.n_tiles > 0)
+    k_scatter<<<a.n_tiles * a.col_split, kScatterThreads, 0, s>>>(a, (const uint4*)x, idx, b);
   else if (a.p2p) k_signal<<<1, 32, 0, s>>>(a, b, 1);
 }
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
@@ -502,7 +517,7 @@ void launch_wait(const unsigned* flags, int n, unsigned epoch, int* err, cudaStr
 }
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s) {
   if (a.n_tiles <= 0) return;
-  auto go = [&](auto kern) { kern<<<a.n_tiles, kScatterThreads, 0, s>>>(a, w, b, (uint4*)out); };
+  auto go = [&](auto kern) { kern<<<a.n_tiles * a.col_split, kScatterThreads, 0, s>>>(a, w, b, (uint4*)out); };
   switch (a.k) {
     case 1: go(k_combine<1>); break;
     case 2: go(k_combine<2>); break;

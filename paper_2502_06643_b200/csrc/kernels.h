@@ -32,6 +32,7 @@ struct PlanArgs {
   int p2p;      // 1 = in-kernel NVLink peer stores/loads (real ranks)
   unsigned epoch;  // P2P flag value of this dispatch
   int n_tiles;  // sum over sources of ceil(T_s / kTileTokens)
+  int col_split;  // K3/K8: CTAs per token tile, each copying a slice of the hidden dim
 };
 
 // Device-side plan state (allocated by the context).

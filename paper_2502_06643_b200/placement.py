@@ -73,7 +73,98 @@ def ilp1_exact(load, G):
     return np.array(best_a, dtype=np.int32), best / G
 
 
+def _canonical(assign):
+    """Relabel clusters canonically: the block holding the lowest unassigned
+    expert gets the lowest free id."""
+    mapping, out = {}, []
+    for c in assign:
+        if c not in mapping:
+            mapping[c] = len(mapping)
+        out.append(mapping[c])
+    return out
+
+
+def ilp1_heuristic(load, G):
+    """ILP 1 for instances too large to enumerate: longest-
+    processing-time greedy seeding, then single-expert moves and pairwise
+    swaps while O1 decreases, never emptying a cluster (Eq. 7)."""
+    load = [int(v) for v in load]
+    E = len(load)
+    if not 1 <= G <= E:
+        raise ValueError("ILP 1 needs 1 <= G <= E (Eq. 7)")
+    order = sorted(range(E), key=lambda e: (-load[e], e))
+    assign = [0] * E
+    T = [0] * G
+    size = [0] * G
+    for i, e in enumerate(order):
+        if i < G:
+            c = i                       # every cluster gets one expert first
+        else:
+            c = min(range(G), key=lambda q: (T[q], q))
+        assign[e] = c
+        T[c] += load[e]
+        size[c] += 1
+    total = sum(load)
+
+    def obj(Tv):
+        return sum(abs(G * t - total) for t in Tv)
+
+    best = obj(T)
+    improved = True
+    while improved:
+        improved = False
+        for e in range(E):                      # moves
+            a = assign[e]
+            if size[a] == 1:
+                continue
+            for c in range(G):
+                if c == a:
+                    continue
+                T[a] -= load[e]
+                T[c] += load[e]
+                v = obj(T)
+                if v < best:
+                    best, assign[e] = v, c
+                    size[a] -= 1
+                    size[c] += 1
+                    improved = True
+                    break
+                T[a] += load[e]
+                T[c] -= load[e]
+        for e1 in range(E):                     # swaps
+            for e2 in range(e1 + 1, E):
+                a, b = assign[e1], assign[e2]
+                if a == b:
+                    continue
+                d = load[e1] - load[e2]
+                T[a] -= d
+                T[b] += d
+                v = obj(T)
+                if v < best:
+                    best = v
+                    assign[e1], assign[e2] = b, a
+                    improved = True
+                else:
+                    T[a] += d
+                    T[b] -= d
+    return np.array(_canonical(assign), dtype=np.int32), best / G
+
+
+def stirling2(n, k):
+    """Number of partitions of n items into k non-empty blocks."""
+    S = [[0] * (k + 1) for _ in range(n + 1)]
+    S[0][0] = 1
+    for i in range(1, n + 1):
+        for j in range(1, min(i, k) + 1):
+            S[i][j] = j * S[i - 1][j] + S[i - 1][j - 1]
+    return S[n][k]
+
+
 def balanced(load, G):
-    """Placement used for the 'balanced' benchmark arm: ILP-1 cluster c -> GPU c."""
-    assign, _ = ilp1_exact(load, G)
+    """Placement used for the 'balanced' benchmark arm: ILP-1 cluster c -> GPU c;
+    exact enumeration when at most 10^6 partitions, else the heuristic."""
+    if stirling2(len(load), G) <= 10 ** 6:
+        assign, _ = ilp1_exact(load, G)
+    else:
+        assign, _ = ilp1_heuristic(load, G)
     return assign.astype(np.int32)

@@ -45,6 +45,27 @@ def test_dominates_contiguous():
         assert o1 <= placement.o1_times_G(load, c, 4) / 4 + 1e-9
 
 
+def test_heuristic_never_beats_exact_and_is_valid():
+    rng = np.random.default_rng(5)
+    for E, G in [(6, 2), (8, 4), (9, 3), (10, 4)]:
+        for _ in range(5):
+            load = rng.integers(0, 1000, size=E)
+            a_h, o_h = placement.ilp1_heuristic(load, G)
+            _, o_x = placement.ilp1_exact(load, G)
+            assert o_h >= o_x - 1e-9
+            assert sorted(set(a_h.tolist())) == list(range(G))          # Eq. (7)
+            assert o_h == pytest.approx(placement.o1_times_G(load, a_h, G) / G)
+
+
+def test_heuristic_uniform_is_perfect_and_large_e_is_fast():
+    a, o = placement.ilp1_heuristic([5] * 64, 8)
+    assert o == 0.0 and np.bincount(a).tolist() == [8] * 8
+    load = (1000 / (np.arange(64) + 1.0) ** 1.6).astype(int)
+    a = placement.balanced(load, 4)          # S(64,4) is astronomically large -> heuristic
+    assert len(a) == 64 and sorted(set(a.tolist())) == [0, 1, 2, 3]
+    assert placement.stirling2(8, 4) == 1701
+
+
 def test_skewed_load_isolates_hot_expert():
     # the SURVEY App. A.1 seed-0 counts at s = 1.6
     load = [13514, 7477, 4032, 2562, 1882, 1345, 1085, 871]
