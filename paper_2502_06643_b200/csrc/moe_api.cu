@@ -146,9 +146,10 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.p2p = c->p2p;
   a.epoch = c->epoch;
   a.n_tiles = plan_tiles(T, c->V);
-  // enough CTAs for the HBM/NVLink-bound row copies: ~2 waves of 148 SMs
+  // enough CTAs for the HBM/NVLink-bound row copies, but no partial second wave:
+  // K3/K8 CTAs (512 threads) fit twice per SM, so aim at <= 2 x num_sms CTAs
   const int chunks = c->H / 8;
-  int split = a.n_tiles > 0 ? (2 * c->num_sms + a.n_tiles - 1) / a.n_tiles : 1;
+  int split = a.n_tiles > 0 ? (2 * c->num_sms) / a.n_tiles : 1;
   split = std::max(1, std::min(split, std::min(8, chunks / 32 > 0 ? chunks / 32 : 1)));
   a.col_split = split;
   return a;
