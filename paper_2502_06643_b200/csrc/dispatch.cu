@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
     int r = 0;
     for (int s = 0; s < a.G; ++s) r += ((volatile const int*)cnt)[s * E + e];
     rows_s[e] = r;
-    pad_s[e] = (r + kSegAlign - 1) / kSegAlign * kSegAlign;
+    pad_s[e] = (r + a.seg_align - 1) / a.seg_align * a.seg_align;
     p_s[e] = p;
   }
   __syncthreads();

@@ -398,14 +398,14 @@ int gemm_block_n(int N, bool swiglu) {
   return 64;
 }
 
-int gemm_b_box_rows(int N, bool swiglu) { return gemm_block_n(N, swiglu) / kGemmCG; }
+int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu) / cg; }
 
-template <int BN, bool SWIGLU>
+template <int BN, bool SWIGLU, int CG>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
                                int* err, unsigned* sched, cudaStream_t s) {
-  using C = GemmCfg<BN, kGemmCG>;
-  auto kern = k_grouped_gemm<BN, SWIGLU, kGemmCG>;
+  using C = GemmCfg<BN, CG>;
+  auto kern = k_grouped_gemm<BN, SWIGLU, CG>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -415,13 +415,13 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(tmA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(tmB);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((num_sms / kGemmCG) * kGemmCG);
+  cfg.gridDim = dim3((num_sms / CG) * CG);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kGemmCG;
+  attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -448,18 +448,21 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags, int wait_n,
-                                unsigned epoch, int* err, unsigned* sched, cudaStream_t s) {
+                                int E, int N, int K, bool swiglu, int cg, int num_sms, const unsigned* wait_flags,
+                                int wait_n, unsigned epoch, int* err, unsigned* sched, cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
-#define MOE_GO(BN_, SW_) \
-  launch_impl<BN_, SW_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, s)
-  if (swiglu) {
-    if (bn == 256) return MOE_GO(256, true);
-    return MOE_GO(128, true);
+#define MOE_GO(BN_, SW_, CG_) \
+  launch_impl<BN_, SW_, CG_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, s)
+  if (cg == 2) {
+    if (swiglu) return bn == 256 ? MOE_GO(256, true, 2) : MOE_GO(128, true, 2);
+    if (bn == 256) return MOE_GO(256, false, 2);
+    if (bn == 128) return MOE_GO(128, false, 2);
+    return MOE_GO(64, false, 2);
   }
-  if (bn == 256) return MOE_GO(256, false);
-  if (bn == 128) return MOE_GO(128, false);
-  return MOE_GO(64, false);
+  if (swiglu) return bn == 256 ? MOE_GO(256, true, 1) : MOE_GO(128, true, 1);
+  if (bn == 256) return MOE_GO(256, false, 1);
+  if (bn == 128) return MOE_GO(128, false, 1);
+  return MOE_GO(64, false, 1);
 #undef MOE_GO
 }
 

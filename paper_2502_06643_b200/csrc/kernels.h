@@ -33,6 +33,7 @@ struct PlanArgs {
   unsigned epoch;  // P2P flag value of this dispatch
   int n_tiles;  // sum over sources of ceil(T_s / kTileTokens)
   int col_split;  // K3/K8: CTAs per token tile, each copying a slice of the hidden dim
+  int seg_align;  // expert segments are padded to this many rows (= the GEMM M tile, 128 or 256)
 };
 
 // Device-side plan state (allocated by the context).
@@ -69,13 +70,15 @@ void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H
 
 // K5/K6 grouped GEMM (gemm.cu).
 int gemm_block_n(int N, bool swiglu);
-int gemm_b_box_rows(int N, bool swiglu);  // TMA box rows of the B (weight) operand per CTA
+int gemm_b_box_rows(int N, bool swiglu, int cg);  // TMA box rows of the B (weight) operand per CTA
 int pack_block(int F);
 // Launch the persistent grouped GEMM: D[rows][ldd] for every hosted expert segment.
 // tmA / tmB are CUtensorMap (128 bytes each) built by make_tmap_2d.  If wait_flags is
 // non-NULL the kernel first waits until wait_flags[0..wait_n) >= epoch (P2P arrivals).
+// cg = CTAs per MMA (2: tcgen05 cta_group::2, 256-row tiles; 1: 128-row tiles for
+// small token counts); must match the segment padding of the dispatch layout.
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int num_sms, const unsigned* wait_flags,
+                                int E, int N, int K, bool swiglu, int cg, int num_sms, const unsigned* wait_flags,
                                 int wait_n, unsigned epoch, int* err, unsigned* sched, cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.

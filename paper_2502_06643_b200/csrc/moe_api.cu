@@ -72,6 +72,12 @@ struct moe_ctx {
   unsigned* done_counter = nullptr;
   bool p2p = false;
   unsigned epoch = 0;
+  // GEMM M tile / segment padding: 256 rows (CTA pair) or, when the context's worst
+  // case averages <= 256 routed rows per expert (decode-sized batches), 128 rows on
+  // one CTA -- halving the MMA work spent on padding rows.  Fixed per context so
+  // every rank derives the same receive layout.
+  int seg_align = kSegAlign;
+  int gemm_cg = kGemmCG;
   std::vector<void*> ipc_opened;        // peer mappings to close
 
   // last dispatch
@@ -146,6 +152,7 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.p2p = c->p2p;
   a.epoch = c->epoch;
   a.n_tiles = plan_tiles(T, c->V);
+  a.seg_align = c->seg_align;
   // enough CTAs for the HBM/NVLink-bound row copies, but no partial second wave:
   // K3/K8 CTAs (512 threads) fit twice per SM, so aim at <= 2 x num_sms CTAs
   const int chunks = c->H / 8;
@@ -196,8 +203,16 @@ moe_status moe_placement_contiguous(int32_t E, int32_t G, int32_t* out) {
   return MOE_OK;
 }
 
+static moe_status layout_host_impl(int32_t E, int32_t G, const int32_t* P, const int32_t* cnt, int align,
+                                   int32_t* seg_start, int32_t* recv_base, int32_t* recv_rows, int32_t* send_base);
+
 moe_status moe_layout_host(int32_t E, int32_t G, const int32_t* P, const int32_t* cnt, int32_t* seg_start,
                            int32_t* recv_base, int32_t* recv_rows, int32_t* send_base) {
+  return layout_host_impl(E, G, P, cnt, kSegAlign, seg_start, recv_base, recv_rows, send_base);
+}
+
+static moe_status layout_host_impl(int32_t E, int32_t G, const int32_t* P, const int32_t* cnt, int align,
+                                   int32_t* seg_start, int32_t* recv_base, int32_t* recv_rows, int32_t* send_base) {
   moe_ctx_t ctx = nullptr;
   if (E <= 0 || G <= 0 || !P || !cnt) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   for (int e = 0; e < E; ++e)
@@ -210,7 +225,7 @@ moe_status moe_layout_host(int32_t E, int32_t G, const int32_t* P, const int32_t
       int64_t rows = 0;
       for (int s = 0; s < G; ++s) rows += cnt[s * E + e];
       start[e] = acc;
-      acc += (rows + kSegAlign - 1) / kSegAlign * kSegAlign;
+      acc += (rows + align - 1) / align * align;
       unp += rows;
     }
     if (recv_rows) recv_rows[g] = (int32_t)unp;
@@ -289,7 +304,15 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   int64_t rows;
   if (ctx->virt || G == 1) rows = Tm * k;
   else rows = (int64_t)G * Tm * k;  // every source may send all its items here
-  ctx->cap_rows = rows + (int64_t)E * kSegAlign;
+  if (rows <= (int64_t)256 * E) {   // decode-sized worst case: 128-row tiles on one CTA
+    ctx->seg_align = 128;
+    ctx->gemm_cg = 1;
+  }
+  if (getenv("MOE_GEMM_CG")) {      // tuning / testing override: 1 or 2
+    ctx->gemm_cg = atoi(getenv("MOE_GEMM_CG")) == 1 ? 1 : 2;
+    ctx->seg_align = 128 * ctx->gemm_cg;
+  }
+  ctx->cap_rows = rows + (int64_t)E * ctx->seg_align;
   ctx->send_rows = (!ctx->virt && G > 1) ? Tm * k : 0;
   ctx->max_tiles = plan_tiles((int)Tm, ctx->V) + ctx->V;
 
@@ -560,7 +583,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     const int32_t* P = ctx->P_host.data();
     const int32_t* cnt = ctx->cnt_host.data();
     std::vector<int32_t> recv_base((size_t)G * E);
-    moe_layout_host(E, G, P, cnt, nullptr, recv_base.data(), nullptr, nullptr);
+    layout_host_impl(E, G, P, cnt, ctx->seg_align, nullptr, recv_base.data(), nullptr, nullptr);
     NC(ncclGroupStart());
     // sends: remote experts in key (P[e], e) order; compact send buffer
     int64_t off = 0;
@@ -635,7 +658,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const int H = ctx->H, F = ctx->F;
   const int nw_rows = ctx->virt ? ctx->E : nw;
   if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows) {
-    const int bn1 = gemm_b_box_rows(2 * F, true), bn2 = gemm_b_box_rows(H, false);
+    const int bn1 = gemm_b_box_rows(2 * F, true, ctx->gemm_cg), bn2 = gemm_b_box_rows(H, false, ctx->gemm_cg);
     if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)nw_rows * 2 * F, H, bn1) ||
         !make_tmap_2d(ctx->tmB2, w2, (uint64_t)nw_rows * H, F, bn2))
       return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weights");
@@ -649,11 +672,12 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // P2P: K5 first waits for every source's arrival flag of this dispatch
   const unsigned* wait = ctx->p2p ? ctx->sig->flag_data : nullptr;
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
-                                      ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev, ctx->done_counter + 2, s);
+                                      ctx->gemm_cg, ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev,
+                                      ctx->done_counter + 2, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
-  e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->num_sms,
-                          nullptr, 0, 0, ctx->err_dev, ctx->done_counter + 2, s);
+  e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
+                          ctx->num_sms, nullptr, 0, 0, ctx->err_dev, ctx->done_counter + 2, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
@@ -720,7 +744,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
     const int32_t* P = ctx->P_host.data();
     const int32_t* cnt = ctx->cnt_host.data();
     std::vector<int32_t> recv_base((size_t)G * E);
-    moe_layout_host(E, G, P, cnt, nullptr, recv_base.data(), nullptr, nullptr);
+    layout_host_impl(E, G, P, cnt, ctx->seg_align, nullptr, recv_base.data(), nullptr, nullptr);
     NC(ncclGroupStart());
     for (int src = 0; src < G; ++src) {
       if (src == ctx->me) continue;
@@ -769,7 +793,7 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
   }
   // P2P: per-rank padded layout of the destination rank
   std::vector<int32_t> peer_base((size_t)G * E);
-  moe_layout_host(E, G, ctx->P_host.data(), cnt.data(), nullptr, peer_base.data(), nullptr, nullptr);
+  layout_host_impl(E, G, ctx->P_host.data(), cnt.data(), ctx->seg_align, nullptr, peer_base.data(), nullptr, nullptr);
   if (cnt_out) memcpy(cnt_out, cnt.data(), sizeof(int32_t) * G * E);
   const int32_t* P = ctx->P_host.data();
   // unpadded receive start of (e, s) on rank P[e]; send-order base of (s, e)
@@ -808,7 +832,7 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
         pstart[(size_t)s * E + e] = acc + r;
         r += cnt[(size_t)s * E + e];
       }
-      acc += (r + kSegAlign - 1) / kSegAlign * kSegAlign;
+      acc += (r + ctx->seg_align - 1) / ctx->seg_align * ctx->seg_align;
     }
   }
   // compact send base (remote experts only) of this rank

@@ -200,6 +200,21 @@ def test_layer_parity(cuda_ok, T, H, F, E, k, G, P):
     assert_close_layer(bf16_to_f64(out), ref)
 
 
+@pytest.mark.parametrize("cg", ["1", "2"])
+def test_both_gemm_tile_modes(cuda_ok, cg, monkeypatch):
+    """128-row tiles on one CTA (decode-sized contexts) and 256-row tiles on a
+    CTA pair (tcgen05 cta_group::2) are both checked against the oracle at a
+    size that spans several tiles of either kind."""
+    monkeypatch.setenv("MOE_GEMM_CG", cg)
+    T, H, F, E, k, G = 1100, 256, 512, 8, 2, 2
+    P = [0, 1, 1, 1, 0, 1, 0, 1]
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=17)
+    lay = make_layer(T, H, F, E, k, G)
+    out, idx, w = run_layer(lay, inp, P, G)
+    ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    assert_close_layer(bf16_to_f64(out), ref)
+
+
 def test_placement_invariance_bit_exact(cuda_ok):
     """The GEMM is deterministic (fixed K order, no split-K), so the layer output is
     bit-identical across placements and G (SURVEY §8(c) 'Placement invariance')."""

@@ -38,9 +38,11 @@ def main():
     w13 = moe.pack_w13(torch.stack([q[0] for q in ws]), torch.stack([q[1] for q in ws]))
     w2 = torch.stack([q[2] for q in ws])
     del ws
-    lay = moe.MoeLayer(max_tokens=Tmax, hidden=H, ffn=F, num_experts=E, max_k=k)
     P = [0] * E
     for T in Ts:
+        # one context per batch size: contexts whose worst case averages <= 256 rows
+        # per expert use 128-row GEMM tiles on one CTA (see moe_ctx_create)
+        lay = moe.MoeLayer(max_tokens=T, hidden=H, ffn=F, num_experts=E, max_k=k)
         x = synth.hidden_states(T, H, 1, device=dev)
         logits = synth.zipf_logits(T, E, 1.6, 1, device=dev)
         prev = synth.zipf_logits(T, E, 1.6, 2, device=dev)
@@ -82,12 +84,16 @@ def main():
             step()
         graph = timeit(g.replay)
         same = bool(torch.equal(out.view(torch.int16), ref.view(torch.int16)))
-        # weight bytes the layer must read at least once (the small-T roofline)
-        wbytes = E * 3 * H * F * 2
-        print(json.dumps({"tokens": T, "eager_ms": eager, "graph_ms": graph, "graph_matches_eager": same,
-                          "weights_GB": wbytes / 1e9, "weight_read_GBps_graph": wbytes / (graph * 1e-3) / 1e9}),
-              flush=True)
-    lay.close()
+        # weight bytes of the experts used must be read at least once (the small-T roofline)
+        used = int(torch.unique(idx).numel())
+        wbytes_used = used * 3 * H * F * 2
+        print(json.dumps({"tokens": T, "gemm_tile_rows": 128 if T * k <= 256 * E else 256,
+                          "eager_ms": eager, "graph_ms": graph, "graph_matches_eager": same,
+                          "experts_used": used, "weights_GB": wbytes_used / 1e9,
+                          "weight_read_GBps_graph": wbytes_used / (graph * 1e-3) / 1e9}), flush=True)
+        del g
+        lay.close()
+    del Tmax
 
 
 if __name__ == "__main__":
