@@ -236,6 +236,29 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
       }
       b.base_row[s * E + e] = base;
     }
+    if (a.p2p) {
+      // fused combine: C3 send-order slot bases.  cslot_base[e] = first slot of this
+      // rank's items of expert e; for each hosted segment and source s: the rows of s
+      // inside the segment and the slot of their first item in s's send order.
+      int sb = 0;
+      for (int q = 0; q < E; ++q)
+        if (p_s[q] * E + q < key) sb += ((volatile const int*)cnt)[a.me * E + q];
+      b.cslot_base[e] = sb;
+      if (hosted) {
+        long long row = rstart;
+        for (int s = 0; s < a.G; ++s) {
+          int slot0 = 0;
+          for (int q = 0; q < E; ++q)
+            if (p_s[q] * E + q < key) slot0 += ((volatile const int*)cnt)[s * E + q];
+          const int n = ((volatile const int*)cnt)[s * E + e];
+          int32_t* d = b.seg_src + ((long long)pos_r * a.G + s) * 3;
+          d[0] = (int)row;
+          d[1] = n;
+          d[2] = slot0;
+          row += n;
+        }
+      }
+    }
   }
   if (e == 0) {
     int n = 0, tp = 0, tu = 0;
@@ -293,18 +316,21 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
     if (e >= 0 && wrank == 0) wcnt[warp * E + e] = __popc(m);
     __syncthreads();
     if (i < n) {
-      int row = -1, slot = 0;
+      int row = -1, slot = 0, cslot = -1;
       if (e >= 0) {
         int r = run[e] + wrank;
         for (int w = 0; w < warp; ++w) r += wcnt[w * E + e];
-        row = b.base_row[s * E + e] + b.tile_base[(long long)tile * E + e] + r;
+        const int within = b.tile_base[(long long)tile * E + e] + r;  // stable rank among (s, e) items
+        row = b.base_row[s * E + e] + within;
         slot = item_slot(a, b.P[e]);
+        if (a.p2p) cslot = b.cslot_base[e] + within;
       }
       it.row[i] = row;
       it.slot[i] = (uint8_t)slot;
       if (write_plan) {
         b.row_of_item[(long long)t0 * a.k + i] = row;
         b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
+        if (a.p2p) b.cslot_of_item[(long long)t0 * a.k + i] = cslot;
       }
     }
     __syncthreads();
@@ -400,13 +426,14 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
   const int k = KT > 0 ? KT : a.k;
   const int n = (t1 - t0) * k;
   const int nslots = a.p2p ? a.G : 2;
-  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = b.src_table[q];
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = a.fused ? b.ret_local : b.src_table[q];
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const long long gi = (long long)t0 * k + i;
-    const int v = b.row_of_item[gi];
+    // fused combine: K6 already stored the row into this rank's return buffer at the C3 slot
+    const int v = a.fused ? b.cslot_of_item[gi] : b.row_of_item[gi];
     row_s[i] = v;
     w_s[i] = v < 0 ? 0.f : w[gi];
-    slot_s[i] = b.slot_of_item[gi];
+    slot_s[i] = a.fused ? 0 : b.slot_of_item[gi];
   }
   if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, a.epoch, b.err);
   __syncthreads();

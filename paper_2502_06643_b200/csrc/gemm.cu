@@ -63,9 +63,10 @@ struct SegSmem {
 
 // tile -> (A row of the tile, first weight row of the expert, N tile index)
 __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile_m, int group_m, int tile, int& arow,
-                                            int& wrow, int& ntile) {
+                                            int& wrow, int& ntile, int& seg) {
   int i = 0;
   while (i + 1 < sg.nseg && tile >= sg.tile0[i + 1]) ++i;
+  seg = i;
   const int local = tile - sg.tile0[i];
   const int mt = sg.mtiles[i];
   int mtile;
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
                    int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch, int* err,
-                   unsigned* sched) {
+                   unsigned* sched, const FusedRet fr) {
   using C = GemmCfg<BN, CG>;
   // P2P mode: the A rows arrive over NVLink from every source rank; wait for
   // their arrival flags (system-scope acquire) before any TMA reads them.
@@ -235,8 +236,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           release_tile(seq);
         }
         if (tile >= total_tiles) break;
-        int arow, wrow, nt;
-        decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt);
+        int arow, wrow, nt, seg;
+        decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt, seg);
         const int a_row = arow + (int)crank * 128;
         const int b_row = wrow + nt * BN + (int)crank * C::B_ROWS;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -312,8 +313,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) release_tile(seq);
       if (tile >= total_tiles) break;
-      int arow, wrow, nt;
-      decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt);
+      int arow, wrow, nt, seg;
+      decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt, seg);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const long long grow = arow + (int)crank * 128 + q * 32 + lane;
@@ -342,6 +343,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else {
         uint16_t* drow = D + grow * ldd + (long long)nt * BN;
+        if (fr.enabled) {
+          // fused combine: this row belongs to source s (rows of s are contiguous in
+          // the segment); store it over NVLink into s's return buffer at the item's
+          // send-order slot.  Padding rows have no source and are not stored.
+          drow = nullptr;
+          const int32_t* ss = fr.seg_src + (long long)seg * fr.G * 3;
+          for (int s = 0; s < fr.G; ++s) {
+            const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
+            if (grow >= r0 && grow < r0 + n) {
+              drow = fr.ret_table[s] + ((long long)__ldg(ss + 3 * s + 2) + (grow - r0)) * ldd + (long long)nt * BN;
+              break;
+            }
+          }
+        }
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t v[32];
@@ -350,10 +365,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          uint4* dst = reinterpret_cast<uint4*>(drow + c);
+          if (drow != nullptr) {
+            uint4* dst = reinterpret_cast<uint4*>(drow + c);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
         }
       }
       tc_fence_before();
@@ -367,6 +384,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (fr.enabled) __threadfence_system();  // peer stores visible before the ready flag
   }
 
   tc_fence_before();
@@ -403,7 +421,7 @@ int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu)
 template <int BN, bool SWIGLU, int CG>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
-                               int* err, unsigned* sched, cudaStream_t s) {
+                               int* err, unsigned* sched, const FusedRet& fr, cudaStream_t s) {
   using C = GemmCfg<BN, CG>;
   auto kern = k_grouped_gemm<BN, SWIGLU, CG>;
   static bool configured = false;
@@ -444,15 +462,16 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   if (group_m > 64) group_m = 64;
   if (env_group != 0) group_m = env_group;
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch, err,
-                            sched);
+                            sched, fr);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const unsigned* wait_flags,
-                                int wait_n, unsigned epoch, int* err, unsigned* sched, cudaStream_t s) {
+                                int wait_n, unsigned epoch, int* err, unsigned* sched, const FusedRet& fr,
+                                cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
 #define MOE_GO(BN_, SW_, CG_) \
-  launch_impl<BN_, SW_, CG_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, s)
+  launch_impl<BN_, SW_, CG_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, fr, s)
   if (cg == 2) {
     if (swiglu) return bn == 256 ? MOE_GO(256, true, 2) : MOE_GO(128, true, 2);
     if (bn == 256) return MOE_GO(256, false, 2);

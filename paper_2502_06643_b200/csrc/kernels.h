@@ -34,6 +34,7 @@ struct PlanArgs {
   int n_tiles;  // sum over sources of ceil(T_s / kTileTokens)
   int col_split;  // K3/K8: CTAs per token tile, each copying a slice of the hidden dim
   int seg_align;  // expert segments are padded to this many rows (= the GEMM M tile, 128 or 256)
+  int fused;      // K8 reads the local return buffer at the C3 slot (fused-combine mode)
 };
 
 // Device-side plan state (allocated by the context).
@@ -53,6 +54,20 @@ struct PlanBuffers {
   SigBlock* my_sig;               // (P2P) this rank's signal block
   unsigned* done_counter;         // last-CTA detection in k_scatter
   int* err;
+  // fused combine (P2P): K6 stores each expert-output row straight into the
+  // source rank's return buffer at the item's send-order slot (C3 slot)
+  int32_t* seg_src;               // [E][G][3]: per hosted segment and source: first row, rows, first slot
+  int32_t* cslot_base;            // [E] send-order slot of this rank's first item for expert e
+  int32_t* cslot_of_item;         // [T*k] send-order slot (C3) of every item of this rank
+  const uint4* ret_local;         // this rank's return buffer
+};
+
+// K6 epilogue redirection (fused combine, P2P mode); enabled == 0 -> plain stores.
+struct FusedRet {
+  uint16_t* const* ret_table;     // [G] every rank's return buffer
+  const int32_t* seg_src;         // see PlanBuffers::seg_src
+  int G;
+  int enabled;
 };
 
 int plan_tiles(int T, int V);
@@ -79,7 +94,8 @@ int pack_block(int F);
 // small token counts); must match the segment padding of the dispatch layout.
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const unsigned* wait_flags,
-                                int wait_n, unsigned epoch, int* err, unsigned* sched, cudaStream_t s);
+                                int wait_n, unsigned epoch, int* err, unsigned* sched, const FusedRet& fr,
+                                cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.

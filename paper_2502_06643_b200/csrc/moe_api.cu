@@ -79,6 +79,12 @@ struct moe_ctx {
   int seg_align = kSegAlign;
   int gemm_cg = kGemmCG;
   std::vector<void*> ipc_opened;        // peer mappings to close
+  // fused combine (P2P): K6 stores expert outputs into the sources' return buffers
+  int32_t* seg_src = nullptr;           // [E][G][3]
+  int32_t* cslot_base = nullptr;        // [E]
+  int32_t* cslot_of_item = nullptr;     // [max_tokens * k]
+  uint16_t** ret_table = nullptr;       // device [G]
+  bool ffn_fused = false;               // the last expert FFN already returned its rows
 
   // last dispatch
   bool have_plan = false;
@@ -136,6 +142,10 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.my_sig = c->sig;
   b.done_counter = c->done_counter;
   b.err = c->err_dev;
+  b.seg_src = c->seg_src;
+  b.cslot_base = c->cslot_base;
+  b.cslot_of_item = c->cslot_of_item;
+  b.ret_local = reinterpret_cast<const uint4*>(c->retbuf);
   return b;
 }
 
@@ -153,6 +163,7 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.epoch = c->epoch;
   a.n_tiles = plan_tiles(T, c->V);
   a.seg_align = c->seg_align;
+  a.fused = c->p2p && c->ffn_fused;
   // enough CTAs for the HBM/NVLink-bound row copies, but no partial second wave:
   // K3/K8 CTAs (512 threads) fit twice per SM, so aim at <= 2 x num_sms CTAs
   const int chunks = c->H / 8;
@@ -342,7 +353,11 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->dst_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
             A((void**)&ctx->src_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
             A((void**)&ctx->peer_sig, sizeof(void*) * (size_t)G) &&
-            A((void**)&ctx->sig, sizeof(SigBlock)) && A((void**)&ctx->done_counter, 4 * sizeof(unsigned));
+            A((void**)&ctx->sig, sizeof(SigBlock)) && A((void**)&ctx->done_counter, 4 * sizeof(unsigned)) &&
+            A((void**)&ctx->seg_src, sizeof(int32_t) * 3 * (size_t)E * G) &&
+            A((void**)&ctx->cslot_base, sizeof(int32_t) * (size_t)E) &&
+            A((void**)&ctx->cslot_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
+            A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G);
   if (!ok) return bail(MOE_ERR_CUDA);
   cudaMemset(ctx->sig, 0, sizeof(SigBlock));
   cudaMemset(ctx->done_counter, 0, 4 * sizeof(unsigned));  // [0] scatter last-CTA, [2..3] GEMM scheduler
@@ -375,7 +390,8 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   // slot g = rank g's receive / expert-output buffer, mapped through CUDA IPC
   // (NVLink peer memory), exchanged once here over NCCL.
   {
-    std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr);
+    std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr), ret(G, nullptr);
+    ret[0] = ctx->retbuf;
     dst[0] = ctx->recv;
     dst[1] = ctx->sendbuf;
     src[0] = ctx->ybuf;
@@ -383,9 +399,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     sig[0] = ctx->sig;
     if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
       ctx->p2p = true;
-      cudaIpcMemHandle_t h[3];
+      cudaIpcMemHandle_t h[4];
       if (cudaIpcGetMemHandle(&h[0], ctx->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->ybuf) != cudaSuccess ||
-          cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess) {
+          cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess || cudaIpcGetMemHandle(&h[3], ctx->retbuf) != cudaSuccess) {
         fail(ctx, MOE_ERR_CUDA, "cudaIpcGetMemHandle failed");
         return bail(MOE_ERR_CUDA);
       }
@@ -406,11 +422,12 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
           dst[g] = ctx->recv;
           src[g] = ctx->ybuf;
           sig[g] = ctx->sig;
+          ret[g] = ctx->retbuf;
           continue;
         }
         const cudaIpcMemHandle_t* hg = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * g);
-        void* p[3] = {nullptr, nullptr, nullptr};
-        for (int i = 0; i < 3; ++i) {
+        void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+        for (int i = 0; i < 4; ++i) {
           cudaError_t e = cudaIpcOpenMemHandle(&p[i], hg[i], cudaIpcMemLazyEnablePeerAccess);
           if (e != cudaSuccess) {
             fail(ctx, MOE_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", g, cudaGetErrorString(e));
@@ -421,11 +438,13 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
         dst[g] = p[0];
         src[g] = p[1];
         sig[g] = p[2];
+        ret[g] = p[3];
       }
     }
     if (cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(ctx->src_table, src.data(), sizeof(void*) * src.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(ctx->peer_sig, sig.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaMemcpy(ctx->peer_sig, sig.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(ctx->ret_table, ret.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
       fail(ctx, MOE_ERR_CUDA, "pointer-table upload failed");
       return bail(MOE_ERR_CUDA);
     }
@@ -450,7 +469,7 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
                  ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
-                 ctx->done_counter};
+                 ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -647,6 +666,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const int nw = ctx->n_hosted;
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
+  ctx->ffn_fused = ctx->p2p && !getenv("MOE_NO_FUSED_COMBINE");
   if (nw == 0) {
     if (ctx->p2p) {  // no expert here: still tell every rank "my outputs are ready"
       launch_signal(a, b, 2, s);
@@ -671,13 +691,18 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (rec) CU(cudaEventRecord(ev[0], s));
   // P2P: K5 first waits for every source's arrival flag of this dispatch
   const unsigned* wait = ctx->p2p ? ctx->sig->flag_data : nullptr;
+  const FusedRet plain{nullptr, nullptr, 0, 0};
+  // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
+  // source rank's return buffer at the item's send-order slot -- the combine
+  // all-to-all overlaps the expert GEMM tile by tile
+  const FusedRet fused{ctx->ret_table, ctx->seg_src, ctx->G, ctx->ffn_fused ? 1 : 0};
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
                                       ctx->gemm_cg, ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev,
-                                      ctx->done_counter + 2, s);
+                                      ctx->done_counter + 2, plain, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
   e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
-                          ctx->num_sms, nullptr, 0, 0, ctx->err_dev, ctx->done_counter + 2, s);
+                          ctx->num_sms, nullptr, 0, 0, ctx->err_dev, ctx->done_counter + 2, fused, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
@@ -719,6 +744,7 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
+  ctx->ffn_fused = false;  // identity rows stay in the expert-output buffer; combine pulls them
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
   if (ctx->p2p) {
