@@ -666,7 +666,10 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const int nw = ctx->n_hosted;
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
-  ctx->ffn_fused = ctx->p2p && !getenv("MOE_NO_FUSED_COMBINE");
+  // Fused combine is opt-in: with one 16-byte remote store per row-chunk per thread
+  // the NVLink writes are uncoalesced and K6 slowed down 4x at E64 / 4EP
+  // (profiles/r1_v7_bench_e64_n4_fused.json); the pull combine (K8 over NVLink) is the default.
+  ctx->ffn_fused = ctx->p2p && getenv("MOE_FUSED_COMBINE") != nullptr;
   if (nw == 0) {
     if (ctx->p2p) {  // no expert here: still tell every rank "my outputs are ready"
       launch_signal(a, b, 2, s);
