@@ -39,16 +39,21 @@ constexpr int kGemmThreads = 192;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kSchedRing = 8;  // depth of the tile-scheduler ring
 
-template <int BN, int CG>
+template <int BN, int CG, bool FUSED = false>
 struct GemmCfg {
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (kSmemBudget / STAGE_BYTES) > 8 ? 8 : (kSmemBudget / STAGE_BYTES);
+  // fused-combine epilogue: each epilogue warp stages its 32 output rows (bf16) so
+  // that remote NVLink stores are whole rows written by the 32 lanes together
+  static constexpr int STAGING = FUSED ? 4 * 32 * BN * 2 : 0;
+  static constexpr int BUDGET = kSmemBudget - STAGING;
+  static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*seg table*/ + 512 /*barriers*/;
+  static constexpr int SMEM =
+      STAGES * STAGE_BYTES + STAGING + 1024 /*align*/ + 8192 /*seg table*/ + 512 /*barriers*/;
   static_assert((2 * STAGES + 4 + 2 * kSchedRing) * 8 + 4 + 4 * kSchedRing <= 512, "barrier area");
   static constexpr int TILE_M = 128 * CG;
 };
@@ -90,13 +95,14 @@ __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile
   wrow = sg.wrow[i];
 }
 
-template <int BN, bool SWIGLU, int CG>
+template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
                    int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch, int* err,
                    unsigned* sched, const FusedRet fr) {
-  using C = GemmCfg<BN, CG>;
+  using C = GemmCfg<BN, CG, FUSED>;
+  static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   // P2P mode: the A rows arrive over NVLink from every source rank; wait for
   // their arrival flags (system-scope acquire) before any TMA reads them.
   if (wait_flags != nullptr && threadIdx.x < wait_n) {
@@ -118,6 +124,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   static_assert(sizeof(SegSmem) <= 8192, "segment table");
   SegSmem& sg = *reinterpret_cast<SegSmem*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 8192);
+  uint8_t* staging = smem + C::STAGES * C::STAGE_BYTES + 8192 + 512;  // FUSED: 4 warps x 32 rows x BN bf16
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -341,22 +348,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int i = 0; i < 4; ++i)
             dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
         }
-      } else {
-        uint16_t* drow = D + grow * ldd + (long long)nt * BN;
-        if (fr.enabled) {
-          // fused combine: this row belongs to source s (rows of s are contiguous in
-          // the segment); store it over NVLink into s's return buffer at the item's
-          // send-order slot.  Padding rows have no source and are not stored.
-          drow = nullptr;
-          const int32_t* ss = fr.seg_src + (long long)seg * fr.G * 3;
-          for (int s = 0; s < fr.G; ++s) {
-            const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
-            if (grow >= r0 && grow < r0 + n) {
-              drow = fr.ret_table[s] + ((long long)__ldg(ss + 3 * s + 2) + (grow - r0)) * ldd + (long long)nt * BN;
-              break;
-            }
+      } else if constexpr (FUSED) {
+        // Fused combine: the row belongs to source s (rows of s are contiguous in the
+        // segment) and goes to s's return buffer at the item's send-order slot, over
+        // NVLink.  The warp stages its 32 rows in shared memory (16-byte granules,
+        // XOR-swizzled by row), releases the accumulator, then writes row by row with
+        // all 32 lanes so every NVLink store is a whole contiguous row segment.
+        constexpr int GR = BN / 8;  // 16-byte granules per row
+        uint4* stg = reinterpret_cast<uint4*>(staging) + (size_t)(warp - 2) * 32 * GR;
+        unsigned long long dst_row = 0;
+        const int32_t* ss = fr.seg_src + (long long)seg * fr.G * 3;
+        for (int s = 0; s < fr.G; ++s) {
+          const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
+          if (grow >= r0 && grow < r0 + n) {
+            dst_row = reinterpret_cast<unsigned long long>(
+                fr.ret_table[s] + ((long long)__ldg(ss + 3 * s + 2) + (grow - r0)) * ldd + (long long)nt * BN);
+            break;
           }
         }
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int g = c / 8 + i;
+            stg[lane * GR + (g ^ (lane & (GR - 1)))] =
+                make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]), __uint_as_float(v[8 * i + 1])),
+                           pack_bf16x2(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
+                           pack_bf16x2(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
+                           pack_bf16x2(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // accumulator drained into smem: the MMA may reuse it
+          if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
+#pragma unroll 1
+        for (int r = 0; r < 32; ++r) {
+          const unsigned long long p = __shfl_sync(0xffffffffu, dst_row, r);
+          if (p == 0) continue;  // padding row
+          uint4* dst = reinterpret_cast<uint4*>(p);
+          for (int g = lane; g < GR; g += 32) dst[g] = stg[r * GR + (g ^ (r & (GR - 1)))];
+        }
+        __syncwarp();
+      } else {
+        uint16_t* drow = D + grow * ldd + (long long)nt * BN;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t v[32];
@@ -365,26 +405,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          if (drow != nullptr) {
-            uint4* dst = reinterpret_cast<uint4*>(drow + c);
+          uint4* dst = reinterpret_cast<uint4*>(drow + c);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-          }
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
-        else mbar_arrive(&tempty[acc]);
+      if constexpr (!FUSED) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
       }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
-    if (fr.enabled) __threadfence_system();  // peer stores visible before the ready flag
+    if constexpr (FUSED) __threadfence_system();  // peer stores visible before the ready flag
   }
 
   tc_fence_before();
@@ -418,12 +458,12 @@ int gemm_block_n(int N, bool swiglu) {
 
 int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu) / cg; }
 
-template <int BN, bool SWIGLU, int CG>
+template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
                                int* err, unsigned* sched, const FusedRet& fr, cudaStream_t s) {
-  using C = GemmCfg<BN, CG>;
-  auto kern = k_grouped_gemm<BN, SWIGLU, CG>;
+  using C = GemmCfg<BN, CG, FUSED>;
+  auto kern = k_grouped_gemm<BN, SWIGLU, CG, FUSED>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -470,18 +510,21 @@ cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, i
                                 int wait_n, unsigned epoch, int* err, unsigned* sched, const FusedRet& fr,
                                 cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
-#define MOE_GO(BN_, SW_, CG_) \
-  launch_impl<BN_, SW_, CG_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, fr, s)
+  const bool fused = fr.enabled && !swiglu;
+#define MOE_GO(BN_, SW_, CG_, FU_) \
+  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, fr, s)
+#define MOE_GO2(BN_, CG_) (fused ? MOE_GO(BN_, false, CG_, true) : MOE_GO(BN_, false, CG_, false))
   if (cg == 2) {
-    if (swiglu) return bn == 256 ? MOE_GO(256, true, 2) : MOE_GO(128, true, 2);
-    if (bn == 256) return MOE_GO(256, false, 2);
-    if (bn == 128) return MOE_GO(128, false, 2);
-    return MOE_GO(64, false, 2);
+    if (swiglu) return bn == 256 ? MOE_GO(256, true, 2, false) : MOE_GO(128, true, 2, false);
+    if (bn == 256) return MOE_GO2(256, 2);
+    if (bn == 128) return MOE_GO2(128, 2);
+    return MOE_GO2(64, 2);
   }
-  if (swiglu) return bn == 256 ? MOE_GO(256, true, 1) : MOE_GO(128, true, 1);
-  if (bn == 256) return MOE_GO(256, false, 1);
-  if (bn == 128) return MOE_GO(128, false, 1);
-  return MOE_GO(64, false, 1);
+  if (swiglu) return bn == 256 ? MOE_GO(256, true, 1, false) : MOE_GO(128, true, 1, false);
+  if (bn == 256) return MOE_GO2(256, 1);
+  if (bn == 128) return MOE_GO2(128, 1);
+  return MOE_GO2(64, 1);
+#undef MOE_GO2
 #undef MOE_GO
 }
 
