@@ -343,11 +343,15 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
   }
 }
 
+// mode: 0 every row; (P2P overlap) 1 = rows this rank hosts, plus the plan
+// arrays; 2 = rows for peers only (runs on a side stream next to K5, whose
+// producer waits per tile for the sources it needs), last CTA raises flag_data.
 __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const uint4* __restrict__ x,
-                                                             const int32_t* __restrict__ idx, PlanBuffers b) {
+                                                             const int32_t* __restrict__ idx, PlanBuffers b,
+                                                             int mode) {
   __shared__ TileItems it;
   __shared__ int run[kMaxExperts];
-  __shared__ int wcnt[(kScatterThreads / 32) * kMaxExperts];
+  extern __shared__ int wcnt[];  // [warps][E] (dynamic: small, so mode 2 co-resides with K5)
   __shared__ uint4* dst_s[kMaxWorld];
   __shared__ unsigned last;
   // col_split CTAs share a token tile; each recomputes the (cheap) in-tile
@@ -358,7 +362,13 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
   tile_info(a, tile, s, t0, t1, tile0);
   const int nslots = a.p2p ? a.G : 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) dst_s[q] = b.dst_table[q];
-  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0);
+  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && mode != 2);
+  if (mode != 0) {  // drop the rows the other kernel copies
+    const int n = (t1 - t0) * a.k;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      if (it.row[i] >= 0 && ((it.slot[i] == a.me) != (mode == 1))) it.row[i] = -1;
+    __syncthreads();
+  }
   // copy: (token, 16-byte chunk) pairs, consecutive threads -> consecutive chunks
   const int cpr = a.H / 8;
   const int cw = (cpr + a.col_split - 1) / a.col_split;
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
       }
     }
   }
-  if (a.p2p) {
+  if (a.p2p && mode != 1) {
     // the last CTA to finish raises flag_data[me] on every rank
     __threadfence_system();
     __syncthreads();
@@ -530,10 +540,13 @@ void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s) { k_sc
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s) {
   k_layout<<<1, kMaxExperts, 0, s>>>(a, b, (long long)cap_rows);
 }
-void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, cudaStream_t s) {
+void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
+                    cudaStream_t s) {
+  const size_t smem = sizeof(int) * (kScatterThreads / 32) * a.E;
   if (a.n_tiles > 0)
-    k_scatter<<<a.n_tiles * a.col_split, kScatterThreads, 0, s>>>(a, (const uint4*)x, idx, b);
-  else if (a.p2p) k_signal<<<1, 32, 0, s>>>(a, b, 1);
+    k_scatter<<<a.n_tiles * a.col_split, kScatterThreads, smem, s>>>(a, (const uint4*)x, idx, b, mode);
+  else if (a.p2p && mode != 1)
+    k_signal<<<1, 32, 0, s>>>(a, b, 1);
 }
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
   k_signal<<<1, 32, 0, s>>>(a, b, which);

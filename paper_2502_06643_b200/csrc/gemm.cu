@@ -58,39 +58,57 @@ struct GemmCfg {
   static constexpr int TILE_M = 128 * CG;
 };
 
+// Tiles come in two phases.  Phase A: per segment, the M tiles made only of this
+// rank's own rows (P2P overlap: they are written locally before K5 starts, so
+// they run while the peers' rows are still crossing NVLink).  Phase B: every
+// other M tile.  Without per-tile waits phase A is empty.
 struct SegSmem {
   int nseg;
+  int totalA;
   int row0[kMaxExperts];
   int wrow[kMaxExperts];   // first weight row of the segment's expert
   int mtiles[kMaxExperts];
-  int tile0[kMaxExperts + 1];
+  short mA0[kMaxExperts], mA1[kMaxExperts];  // phase-A M tiles [mA0, mA1)
+  int tA0[kMaxExperts + 1];                 // phase-A tile prefix
+  int tB0[kMaxExperts + 1];                 // phase-B tile prefix
 };
 
-// tile -> (A row of the tile, first weight row of the expert, N tile index)
-__device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile_m, int group_m, int tile, int& arow,
-                                            int& wrow, int& ntile, int& seg) {
-  int i = 0;
-  while (i + 1 < sg.nseg && tile >= sg.tile0[i + 1]) ++i;
-  seg = i;
-  const int local = tile - sg.tile0[i];
-  const int mt = sg.mtiles[i];
-  int mtile;
+// position p among n M tiles of one phase -> (M tile index within the phase, N tile)
+__device__ __forceinline__ void raster(int group_m, int ntn, int n, int local, int& mi, int& ntile) {
   if (group_m > 0) {  // groups of group_m M tiles, N outer, M fastest (A group L2-resident)
     const int per_group = group_m * ntn;
     const int g = local / per_group;
     const int r = local % per_group;
-    const int gm = min(group_m, mt - g * group_m);  // M tiles in this group
+    const int gm = min(group_m, n - g * group_m);  // M tiles in this group
     ntile = r / gm;
-    mtile = g * group_m + r % gm;
+    mi = g * group_m + r % gm;
   } else {            // groups of -group_m N tiles, M outer, N fastest (weight group L2-resident)
     const int gfull = -group_m;
-    const int per_group = gfull * mt;
+    const int per_group = gfull * n;
     const int g = local / per_group;
     const int r = local % per_group;
     const int gn = min(gfull, ntn - g * gfull);
-    mtile = r / gn;
+    mi = r / gn;
     ntile = g * gfull + r % gn;
   }
+}
+
+// tile -> (A row of the tile, first weight row of the expert, N tile index, segment)
+__device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile_m, int group_m, int tile, int& arow,
+                                            int& wrow, int& ntile, int& seg) {
+  int i = 0, mtile, mi;
+  if (tile < sg.totalA) {
+    while (i + 1 < sg.nseg && tile >= sg.tA0[i + 1]) ++i;
+    raster(group_m, ntn, sg.mA1[i] - sg.mA0[i], tile - sg.tA0[i], mi, ntile);
+    mtile = sg.mA0[i] + mi;
+  } else {
+    const int t = tile - sg.totalA;
+    while (i + 1 < sg.nseg && t >= sg.tB0[i + 1]) ++i;
+    const int nA = sg.mA1[i] - sg.mA0[i];
+    raster(group_m, ntn, sg.mtiles[i] - nA, t - sg.tB0[i], mi, ntile);
+    mtile = mi < sg.mA0[i] ? mi : mi + nA;
+  }
+  seg = i;
   arow = sg.row0[i] + mtile * tile_m;
   wrow = sg.wrow[i];
 }
@@ -99,24 +117,9 @@ template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m, const unsigned* __restrict__ wait_flags, int wait_n, unsigned epoch, int* err,
-                   unsigned* sched, const FusedRet fr) {
+                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
-  // P2P mode: the A rows arrive over NVLink from every source rank; wait for
-  // their arrival flags (system-scope acquire) before any TMA reads them.
-  if (wait_flags != nullptr && threadIdx.x < wait_n) {
-    unsigned v;
-    const unsigned long long t0 = globaltimer_ns();
-    do {
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_flags + threadIdx.x) : "memory");
-      if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
-        atomicOr(err, kErrTimeout);
-        break;
-      }
-    } while ((int)(v - epoch) < 0);
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy arrivals -> TMA (async proxy)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -147,17 +150,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0) {
     const int nseg = seg_meta[0];
     sg.nseg = nseg;
-    int acc = 0;
+    int accA = 0, accB = 0;
     for (int i = 0; i < nseg; ++i) {
       const int rows = seg_meta[1 + E + i];
       const int mt = (rows + C::TILE_M - 1) / C::TILE_M;
       sg.row0[i] = seg_meta[1 + i];
       sg.wrow[i] = seg_meta[1 + 2 * E + i] * N;
       sg.mtiles[i] = mt;
-      sg.tile0[i] = acc;
-      acc += mt * ntn;
+      int a0 = 0, a1 = 0;
+      if (sw.flags != nullptr) {  // M tiles lying inside this rank's own rows [lo, hi)
+        const int32_t* own = sw.seg_src + ((long long)i * sw.G + sw.me) * 3;
+        const int lo = own[0] - sg.row0[i], hi = lo + own[1];
+        if (own[1] > 0) {
+          a0 = min(mt, (lo + C::TILE_M - 1) / C::TILE_M);
+          a1 = hi >= rows ? mt : hi / C::TILE_M;
+          if (a1 < a0) a1 = a0;
+        }
+      }
+      sg.mA0[i] = (short)a0;
+      sg.mA1[i] = (short)a1;
+      sg.tA0[i] = accA;
+      sg.tB0[i] = accB;
+      accA += (a1 - a0) * ntn;
+      accB += (mt - (a1 - a0)) * ntn;
     }
-    sg.tile0[nseg] = acc;
+    sg.tA0[nseg] = accA;
+    sg.tB0[nseg] = accB;
+    sg.totalA = accA;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -196,7 +215,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total_tiles = sg.tile0[sg.nseg];
+  const int total_tiles = sg.totalA + sg.tB0[sg.nseg];
 
   // Dynamic tile scheduler: the leader's producer takes the next tile id from a
   // global counter (atomicAdd) and publishes it through an mbarrier ring to
@@ -225,6 +244,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int seq = 0;
+      unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
       while (true) {
         int tile;
         if (leader) {
@@ -247,6 +267,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt, seg);
         const int a_row = arow + (int)crank * 128;
         const int b_row = wrow + nt * BN + (int)crank * C::B_ROWS;
+        if (sw.flags != nullptr) {
+          // P2P overlap: wait for the source ranks whose rows this CTA's half of the
+          // tile holds (system-scope acquire of their arrival flags), then order
+          // those generic-proxy arrivals before the TMA (async proxy) reads
+          const int32_t* ss = sw.seg_src + (long long)seg * sw.G * 3;
+          bool waited = false;
+          for (int s = 0; s < sw.G; ++s) {
+            if (s == sw.me || ((ready >> s) & 1ull)) continue;
+            const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
+            if (n == 0 || r0 >= a_row + 128 || r0 + n <= a_row) continue;
+            const unsigned long long t0 = globaltimer_ns();
+            unsigned v;
+            do {
+              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sw.flags + s) : "memory");
+              if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
+                atomicOr(err, kErrTimeout);
+                break;
+              }
+            } while ((int)(v - sw.epoch) < 0);
+            ready |= 1ull << s;
+            waited = true;
+          }
+          if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
@@ -460,8 +504,8 @@ int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu)
 
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
-                               int N, int K, int num_sms, const unsigned* wait_flags, int wait_n, unsigned epoch,
-                               int* err, unsigned* sched, const FusedRet& fr, cudaStream_t s) {
+                               int N, int K, int num_sms, const SrcWait& sw, int* err, unsigned* sched,
+                               const FusedRet& fr, cudaStream_t s) {
   using C = GemmCfg<BN, CG, FUSED>;
   auto kern = k_grouped_gemm<BN, SWIGLU, CG, FUSED>;
   static bool configured = false;
@@ -501,18 +545,17 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   if (group_m < 1) group_m = 1;
   if (group_m > 64) group_m = 64;
   if (env_group != 0) group_m = env_group;
-  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, wait_flags, wait_n, epoch, err,
+  return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
                             sched, fr);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int cg, int num_sms, const unsigned* wait_flags,
-                                int wait_n, unsigned epoch, int* err, unsigned* sched, const FusedRet& fr,
-                                cudaStream_t s) {
+                                int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
+                                unsigned* sched, const FusedRet& fr, cudaStream_t s) {
   const int bn = gemm_block_n(N, swiglu);
   const bool fused = fr.enabled && !swiglu;
 #define MOE_GO(BN_, SW_, CG_, FU_) \
-  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, wait_flags, wait_n, epoch, err, sched, fr, s)
+  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s)
 #define MOE_GO2(BN_, CG_) (fused ? MOE_GO(BN_, false, CG_, true) : MOE_GO(BN_, false, CG_, false))
   if (cg == 2) {
     if (swiglu) return bn == 256 ? MOE_GO(256, true, 2, false) : MOE_GO(128, true, 2, false);

@@ -62,6 +62,16 @@ struct PlanBuffers {
   const uint4* ret_local;         // this rank's return buffer
 };
 
+// K5 per-tile arrival waits (P2P overlap): the producer waits only for the source
+// ranks whose rows a tile reads; tiles holding only this rank's own rows run first.
+struct SrcWait {
+  const unsigned* flags;          // flag_data[G] of this rank; nullptr = no waits (all rows local)
+  const int32_t* seg_src;         // see PlanBuffers::seg_src
+  int G;
+  int me;
+  unsigned epoch;
+};
+
 // K6 epilogue redirection (fused combine, P2P mode); enabled == 0 -> plain stores.
 struct FusedRet {
   uint16_t* const* ret_table;     // [G] every rank's return buffer
@@ -74,7 +84,9 @@ int plan_tiles(int T, int V);
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
 void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s);
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s);
-void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
+// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers
+void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
+                    cudaStream_t s);
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s);
 // P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);
@@ -93,9 +105,8 @@ int pack_block(int F);
 // cg = CTAs per MMA (2: tcgen05 cta_group::2, 256-row tiles; 1: 128-row tiles for
 // small token counts); must match the segment padding of the dispatch layout.
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int cg, int num_sms, const unsigned* wait_flags,
-                                int wait_n, unsigned epoch, int* err, unsigned* sched, const FusedRet& fr,
-                                cudaStream_t s);
+                                int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
+                                unsigned* sched, const FusedRet& fr, cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.

@@ -85,6 +85,10 @@ struct moe_ctx {
   int32_t* cslot_of_item = nullptr;     // [max_tokens * k]
   uint16_t** ret_table = nullptr;       // device [G]
   bool ffn_fused = false;               // the last expert FFN already returned its rows
+  // P2P overlap: rows for peers are pushed on a side stream while K5 starts on
+  // this rank's own rows (fork after the layout kernel, join in combine)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // last dispatch
   bool have_plan = false;
@@ -399,6 +403,12 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     sig[0] = ctx->sig;
     if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
       ctx->p2p = true;
+      if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        fail(ctx, MOE_ERR_CUDA, "side stream / event creation failed");
+        return bail(MOE_ERR_CUDA);
+      }
       cudaIpcMemHandle_t h[4];
       if (cudaIpcGetMemHandle(&h[0], ctx->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->ybuf) != cudaSuccess ||
           cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess || cudaIpcGetMemHandle(&h[3], ctx->retbuf) != cudaSuccess) {
@@ -466,6 +476,9 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
     ncclCommDestroy(ctx->comm);
   }
   for (void* p : ctx->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
                  ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
@@ -582,7 +595,11 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->me);
   ctx->n_hosted = n_hosted;
 
-  if (ctx->p2p) ++ctx->epoch;
+  if (ctx->p2p) {
+    ++ctx->epoch;
+    // the previous layer's side-stream scatter reads plan arrays this call rewrites
+    CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  }
   PlanArgs a = plan_args(ctx, T, k);
   PlanBuffers b = plan_buffers(ctx);
   launch_count(a, idx, b, s);
@@ -596,8 +613,19 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     memcpy(ctx->cnt_host.data(), ctx->cnt_pinned, sizeof(int32_t) * G * E);
   }
   launch_layout(a, b, ctx->cap_rows, s);  // P2P: also the in-kernel count all-gather
-  launch_scatter(a, x, idx, b, s);        // P2P: NVLink stores into the hosting rank + arrival flags
-  LAUNCHED(ctx, 2);
+  if (ctx->p2p) {
+    // rows for peers: NVLink stores on the side stream (arrival flags raised by its
+    // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
+    CU(cudaEventRecord(ctx->ev_fork, s));
+    CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    launch_scatter(a, x, idx, b, 2, ctx->side);
+    CU(cudaEventRecord(ctx->ev_join, ctx->side));
+    launch_scatter(a, x, idx, b, 1, s);
+    LAUNCHED(ctx, 3);
+  } else {
+    launch_scatter(a, x, idx, b, 0, s);
+    LAUNCHED(ctx, 2);
+  }
   if (nccl) {
     const int32_t* P = ctx->P_host.data();
     const int32_t* cnt = ctx->cnt_host.data();
@@ -698,20 +726,22 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const bool rec = ctx->timing_used < (int)ctx->ev.size() / 3;
   cudaEvent_t* ev = rec ? &ctx->ev[3 * ctx->timing_used] : nullptr;
   if (rec) CU(cudaEventRecord(ev[0], s));
-  // P2P: K5 first waits for every source's arrival flag of this dispatch
-  const unsigned* wait = ctx->p2p ? ctx->sig->flag_data : nullptr;
+  // P2P: K5's producer waits per tile for the source ranks whose rows the tile reads;
+  // the tiles of this rank's own rows go first (overlapping the peers' NVLink pushes)
+  const SrcWait wait1{ctx->p2p ? ctx->sig->flag_data : nullptr, ctx->seg_src, ctx->G, ctx->me, ctx->epoch};
+  const SrcWait nowait{nullptr, nullptr, 0, 0, 0};
   const FusedRet plain{nullptr, nullptr, 0, 0};
   // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
   // source rank's return buffer at the item's send-order slot -- the combine
   // all-to-all overlaps the expert GEMM tile by tile
   const FusedRet fused{ctx->ret_table, ctx->seg_src, ctx->G, ctx->ffn_fused ? 1 : 0};
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
-                                      ctx->gemm_cg, ctx->num_sms, wait, ctx->G, ctx->epoch, ctx->err_dev,
-                                      ctx->done_counter + 2, plain, s);
+                                      ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
+                                      s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
   e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
-                          ctx->num_sms, nullptr, 0, 0, ctx->err_dev, ctx->done_counter + 2, fused, s);
+                          ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
@@ -757,6 +787,9 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
   if (ctx->p2p) {
+    // join the side-stream scatter first (never spin on a flag another kernel of
+    // this GPU raises), then wait for the peers' rows
+    CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, ctx->err_dev, s);
     LAUNCHED(ctx, 1);
   }
@@ -806,6 +839,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   PlanBuffers b = plan_buffers(ctx);
   launch_combine(a, w, b, out, s);
   LAUNCHED(ctx, a.n_tiles > 0);
+  if (ctx->p2p) CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));  // join the side stream
   return MOE_OK;
 }
 
