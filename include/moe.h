@@ -97,7 +97,9 @@ moe_status moe_get_unique_id(uint8_t out[128]);
 
 /* Create a context (collective over the EP group when world > 1).  Allocates
  * every workspace for the worst case of dropless routing (G6): per process
- * max_tokens * min(k, E_local) routed rows plus 128-row padding per expert.
+ * max_tokens * min(k, E_local) routed rows plus per-expert padding to the GEMM
+ * M tile (256 rows; 128 rows for decode-sized contexts whose worst case averages
+ * <= 256 routed rows per expert -- they run the GEMM on 128-row tiles).
  * uid: host, 128 bytes from moe_get_unique_id, or NULL when world == 1. */
 moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out);
 moe_status moe_ctx_destroy(moe_ctx_t ctx);               /* collective when world > 1 */
@@ -136,7 +138,7 @@ moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int
  * expert_to_rank: HOST int32 [E], values in [0, G) (the placement input; a rank
  * may host 0 experts).  Builds the stable send order (key P[e], e, t), the
  * expert-major receive layout (e ascending on g, then source s, then t; each
- * expert segment padded to 128 rows) and moves every routed row to the rank
+ * expert segment padded to the GEMM M tile) and moves every routed row to the rank
  * hosting its expert.  Collective when world > 1 (NCCL mode synchronises the
  * stream once to read the G x E count matrix).  The plan stays in the context
  * until the next moe_dispatch.  info: host, optional; if non-NULL the call
