@@ -558,7 +558,7 @@ def main():
                     help="all-to-all transport between real ranks (N > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=2048)
-    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=32)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
