@@ -117,7 +117,7 @@ template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr) {
+                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   extern __shared__ uint8_t smem_raw[];
@@ -245,12 +245,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int seq = 0;
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
+      // the next tile id is fetched one tile ahead, so the global atomic's latency
+      // overlaps this tile's loads instead of stalling the MMA at the tile switch
+      int next_tile = leader ? (int)atomicAdd(sched, 1u) : 0;
       while (true) {
         int tile;
         if (leader) {
           const int slot = seq % kSchedRing;
           mbar_wait_cluster(&sempty[slot], (uint32_t)(((seq / kSchedRing) & 1) ^ 1));
-          tile = (int)atomicAdd(sched, 1u);
+          tile = next_tile;
+          if (tile < total_tiles) next_tile = (int)atomicAdd(sched, 1u);
           sched_tile[slot] = tile;
           if constexpr (CG == 2) {
             st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)tile);
@@ -291,7 +295,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        // L2 prefetch `pf` k-blocks ahead of the loads: the first cluster to touch a
+        // weight tile would otherwise stall on DRAM latency for each of its k-blocks
+        for (int kb = 0; kb < min(pf, nkb); ++kb) {
+          tma_prefetch_l2_2d(&tmA, kb * BK, a_row);
+          tma_prefetch_l2_2d(&tmB, kb * BK, b_row);
+        }
         for (int kb = 0; kb < nkb; ++kb) {
+          if (kb + pf < nkb) {
+            tma_prefetch_l2_2d(&tmA, (kb + pf) * BK, a_row);
+            tma_prefetch_l2_2d(&tmB, (kb + pf) * BK, b_row);
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -545,8 +559,14 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   if (group_m < 1) group_m = 1;
   if (group_m > 64) group_m = 64;
   if (env_group != 0) group_m = env_group;
+  static int pf = -1;  // L2 prefetch distance in k-blocks (MOE_GEMM_PREFETCH, tuning)
+  if (pf < 0) {
+    const char* env = getenv("MOE_GEMM_PREFETCH");
+    pf = env ? atoi(env) : 0;
+    if (pf < 0) pf = 0;
+  }
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
-                            sched, fr);
+                            sched, fr, pf);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
