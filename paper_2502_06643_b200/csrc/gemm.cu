@@ -117,7 +117,8 @@ template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf) {
+                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf,
+                   int tile_ahead) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   extern __shared__ uint8_t smem_raw[];
@@ -245,16 +246,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int seq = 0;
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
-      // the next tile id is fetched one tile ahead, so the global atomic's latency
-      // overlaps this tile's loads instead of stalling the MMA at the tile switch
-      int next_tile = leader ? (int)atomicAdd(sched, 1u) : 0;
+      // (tile_ahead) the next tile id may be fetched one tile ahead, so the global
+      // atomic's latency overlaps this tile's loads; off by default (measured slower)
+      int next_tile = (leader && tile_ahead) ? (int)atomicAdd(sched, 1u) : 0;
       while (true) {
         int tile;
         if (leader) {
           const int slot = seq % kSchedRing;
           mbar_wait_cluster(&sempty[slot], (uint32_t)(((seq / kSchedRing) & 1) ^ 1));
-          tile = next_tile;
-          if (tile < total_tiles) next_tile = (int)atomicAdd(sched, 1u);
+          if (tile_ahead) {
+            tile = next_tile;
+            if (tile < total_tiles) next_tile = (int)atomicAdd(sched, 1u);
+          } else {
+            tile = (int)atomicAdd(sched, 1u);
+          }
           sched_tile[slot] = tile;
           if constexpr (CG == 2) {
             st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)tile);
@@ -565,8 +570,13 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
     pf = env ? atoi(env) : 0;
     if (pf < 0) pf = 0;
   }
+  static int ahead = -1;  // MOE_GEMM_TILE_AHEAD=1: fetch tile ids one tile ahead (tuning)
+  if (ahead < 0) {
+    const char* env = getenv("MOE_GEMM_TILE_AHEAD");
+    ahead = (env && atoi(env) != 0) ? 1 : 0;
+  }
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
-                            sched, fr, pf);
+                            sched, fr, pf, ahead);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
