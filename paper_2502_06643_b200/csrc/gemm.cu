@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_prefetch_l2_2d(&tmB, kb * BK, b_row);
         }
         for (int kb = 0; kb < nkb; ++kb) {
-          if (kb + pf < nkb) {
+          if (pf > 0 && kb + pf < nkb) {
             tma_prefetch_l2_2d(&tmA, (kb + pf) * BK, a_row);
             tma_prefetch_l2_2d(&tmB, (kb + pf) * BK, b_row);
           }
