@@ -37,15 +37,20 @@ def validate_placement(P, G):
 
 
 def plan(idx_by_source, P, G):
-    """C3 for G source ranks.
+    """C3 for S = len(idx_by_source) source ranks and G destination ranks.
+
+    S == G for plain expert parallelism.  With tensor parallelism inside the
+    experts (reading G20, `layer.layer_ep_tp`) every one of the S = G * tp ranks
+    is a source and the destinations are the G EP groups; every rank of group g
+    receives the same rows, in the receive order below.
 
     idx_by_source[s]: int [T_s][k] expert ids of source s's tokens.
-    P: int [E] expert -> rank.
+    P: int [E] expert -> rank (EP group).
 
     Returns a dict with
       slot[s]       int [T_s][k]  position of item (t, j) in source s's send order
-      cnt           int [G][E]    cnt[s][e] = items of s routed to e
-      send_counts   int [G][G]    send_counts[s][g] = sum_{P[e]=g} cnt[s][e]
+      cnt           int [S][E]    cnt[s][e] = items of s routed to e
+      send_counts   int [S][G]    send_counts[s][g] = sum_{P[e]=g} cnt[s][e]
       recv_counts   int [G]       rows received by rank g
       recv[g]       list of (s, t, j, e) in rank g's receive order
       recv_pos[s]   int [T_s][k]  position of item (t, j) of s in recv[P[e]]
@@ -53,10 +58,10 @@ def plan(idx_by_source, P, G):
     P = np.asarray(P, dtype=np.int64)
     E = len(P)
     validate_placement(P, G)
-    assert len(idx_by_source) == G
-    cnt = np.zeros((G, E), dtype=np.int64)
+    S = len(idx_by_source)
+    cnt = np.zeros((S, E), dtype=np.int64)
     slot = []
-    for s in range(G):
+    for s in range(S):
         idx = np.asarray(idx_by_source[s])
         T_s, k = idx.shape
         items = [(t, j) for t in range(T_s) for j in range(k)]     # flattened order
@@ -68,18 +73,18 @@ def plan(idx_by_source, P, G):
         slot.append(sl)
         for (t, j) in items:
             cnt[s, idx[t, j]] += 1
-    send_counts = np.zeros((G, G), dtype=np.int64)
-    for s in range(G):
+    send_counts = np.zeros((S, G), dtype=np.int64)
+    for s in range(S):
         for e in range(E):
             send_counts[s, P[e]] += cnt[s, e]
     recv = []
-    recv_pos = [np.full(np.asarray(idx_by_source[s]).shape, -1, dtype=np.int64) for s in range(G)]
+    recv_pos = [np.full(np.asarray(idx_by_source[s]).shape, -1, dtype=np.int64) for s in range(S)]
     for g in range(G):
         rows = []
         for e in range(E):
             if P[e] != g:
                 continue
-            for s in range(G):
+            for s in range(S):
                 idx = np.asarray(idx_by_source[s])
                 for t in range(idx.shape[0]):
                     for j in range(idx.shape[1]):
