@@ -214,8 +214,14 @@ def run_ours(args):
     t0, t1 = bl[rank]
     Tr = t1 - t0
     Tmax = max(b - a for a, b in bl)
+    tp = args.tp
+    if N % tp:
+        raise SystemExit(f"--tp {tp} must divide --gpus {N}")
+    G = N // tp                 # EP groups (= EP ranks when tp == 1)
+    grp, tpq = rank // tp, rank % tp
+    Fl = F // tp                # FFN columns this rank computes (TP slice, reading G20)
     lay = moe.MoeLayer(max_tokens=max(Tmax, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N, rank=rank,
-                       device=local, uid=uid, a2a=args.a2a)
+                       device=local, uid=uid, a2a=args.a2a, tp=tp)
     s = args.zipf_s
     x = synth.hidden_states(T, H, args.seed, device=dev)[t0:t1].contiguous()
     logits = synth.zipf_logits(T, E, s, args.seed, device=dev)[t0:t1].contiguous()
@@ -231,18 +237,18 @@ def run_ours(args):
     # GPU's own routing statistics (profile -> ILP -> placement)
     placements = {}
     if args.placement in ("contiguous", "both"):
-        placements["contiguous"] = moe.placement_contiguous(E, N)
-    if args.placement in ("balanced", "both") and (N > 1 or args.placement == "balanced"):
+        placements["contiguous"] = moe.placement_contiguous(E, G)
+    if args.placement in ("balanced", "both") and (G > 1 or args.placement == "balanced"):
         prof_load = torch.zeros(E, dtype=torch.int64, device=dev)
         pidx, _ = lay.route(logits, k)
         lay.route_stats(pidx, None, prof_load, None)
         lay.stats_allreduce(prof_load, None)
         lay.sync()
-        placements["balanced"] = placement.balanced(prof_load.cpu().numpy(), N).astype(np.int32)
+        placements["balanced"] = placement.balanced(prof_load.cpu().numpy(), G).astype(np.int32)
 
     weights = {}
     for name, P in placements.items():
-        hosted = [e for e in range(E) if P[e] == rank]
+        hosted = [e for e in range(E) if P[e] == grp]
         if not hosted:
             weights[name] = (None, None)
             continue
@@ -251,7 +257,10 @@ def run_ours(args):
         w3 = torch.stack([q[1] for q in ws])
         w2 = torch.stack([q[2] for q in ws])
         del ws
-        w13 = moe.pack_w13(w1, w3)
+        if tp > 1:     # this rank's FFN slice of its group's experts
+            w13, w2 = moe.tp_slice_weights(w1, w3, w2, tp, tpq)
+        else:
+            w13 = moe.pack_w13(w1, w3)
         del w1, w3
         weights[name] = (w13, w2)
     torch.cuda.synchronize()
@@ -323,7 +332,7 @@ def run_ours(args):
         per_step_mean = mean_over_ranks(per_step)
         total_max = float(max_over_ranks([total])[0])
         rows_here = int(info.recv_rows) if info is not None else 0
-        recv_counts = list(info.recv_counts)[:N]
+        recv_counts = list(info.recv_counts)[:G]
         res = dict(
             total_ms=total_max, ms_per_step=total_max / args.steps,
             p50_ms=float(np.percentile(per_step_max, 50)), p99_ms=float(np.percentile(per_step_max, 99)),
@@ -364,8 +373,9 @@ def run_ours(args):
             "all_to_all_avg": float(mean_over_ranks([pm[2] + pm[4]])[0])}
         if N > 1:
             # NVLink traffic this rank drives per phase: its remote routed rows x 2H bytes
-            # (dispatch pushes them to the hosting ranks, combine pulls them back)
-            sent = sum(int(info.send_counts[g]) for g in range(N) if g != rank)
+            # (dispatch pushes them to the hosting ranks, combine pulls them back); with
+            # tp > 1 every row goes to the tp ranks of its group (one of them may be us)
+            sent = sum(int(info.send_counts[g]) * (tp if g != grp else tp - 1) for g in range(G))
             nv_bytes = sent * 2 * H
             bw = [nv_bytes / (pm[2] * 1e-3) / 1e9, nv_bytes / (pm[4] * 1e-3) / 1e9]
             res["nvlink"] = {"remote_bytes_per_phase_rank0": nv_bytes,
@@ -462,20 +472,20 @@ def run_ours(args):
     if rank == 0:
         r = results[head]
         R = r["rows_rank0"]
-        flops_k5 = 4.0 * H * F * R
+        flops_k5 = 4.0 * H * Fl * R
         peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
         ach = flops_k5 / (r["k5_ms"] * 1e-3) / 1e12 if r["k5_ms"] else None
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
-            tj = json.load(open(tp))
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath) and tp == 1:
+            tj = json.load(open(tpath))
             traffic = tj.get(f"{args.config}_N{N}_{head}", {}).get("k5_dram_bytes")
         line = {
             "metric": METRIC, "value": r["tokens_per_s"], "unit": "tokens/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded Zipf logits, N(0,1) tokens, random-init weights)",
             "config": {"workload": cfg["workload"], "experts": E, "top_k": k, "hidden": H, "ffn": F,
-                       "tokens_total": T, "ep": N, "placement": head, "zipf_s": s, "seed": args.seed,
+                       "tokens_total": T, "ep": G, "tp": tp, "placement": head, "zipf_s": s, "seed": args.seed,
                        "a2a": args.a2a if N > 1 else "none (single GPU)",
                        "l2": "no flush: inputs larger than L2 (expert weights 2.8 GB, activations 128 MiB)"
                        if args.config == "mixtral" else "no flush"},
@@ -490,7 +500,7 @@ def run_ours(args):
                          "peak_source": peaks_src + " bf16 sustained (kernel timed inside a long step)",
                          "frac_of_burst": (ach / peaks.get("bf16_tflops")) if ach else None,
                          "k6_ms": r["k6_ms"],
-                         "k6_frac": (2.0 * H * F * R / (r["k6_ms"] * 1e-3) / 1e12 / peak) if r["k6_ms"] else None},
+                         "k6_frac": (2.0 * H * Fl * R / (r["k6_ms"] * 1e-3) / 1e12 / peak) if r["k6_ms"] else None},
             "clocks": r["clocks"],
             "placements": {n: {kk: v for kk, v in res.items() if kk not in ("clocks",)} for n, res in results.items()},
             "stats_pass": {"layers": L, "tokens_total": T, "ms": stats_ms, "us_per_layer": stats_ms * 1e3 / L,
@@ -556,6 +566,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--a2a", choices=["nccl", "p2p"], default="p2p",
                     help="all-to-all transport between real ranks (N > 1)")
+    ap.add_argument("--tp", type=int, default=1,
+                    help="tensor-parallel ranks per expert (EP groups = gpus / tp; reading G20)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=2048)
     ap.add_argument("--cpu-reps", type=int, default=3)

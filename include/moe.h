@@ -32,6 +32,16 @@
  * floor(T/G) + [s < T mod G] tokens.  In virtual mode the T passed to a call
  * covers all G ranks' tokens concatenated in rank order; in real mode T is
  * this rank's own token count (may differ per rank, may be 0).
+ *
+ * Tensor parallelism inside the experts (config.tp > 1; the paper's "4EP-2TP",
+ * P:L77-79; reading G20): the G ranks form G/tp EP groups of tp
+ * consecutive ranks (rank r = TP index r % tp of group r / tp).  Every rank owns
+ * a token block and is a source; the placement maps experts to EP GROUPS; every
+ * rank of group g receives all rows routed to g's experts (the TP all-gather is
+ * part of the dispatch) and computes the slice of the FFN dimension its TP index
+ * owns; the bf16 partial outputs go back to the source, which sums the tp
+ * partials (fp32, TP index ascending) before the gate-weighted combine (the TP
+ * reduce-scatter is part of the combine).
  */
 #ifndef MOE_H
 #define MOE_H
@@ -69,7 +79,7 @@ typedef struct {
   int32_t rank;           /* this process's rank in [0, world) */
   int32_t device;         /* CUDA device ordinal */
   int32_t virtual_ranks;  /* >1 => emulate that many EP ranks (world must be 1) */
-  int32_t a2a_mode;       /* moe_a2a_mode (real ranks only):
+  int32_t a2a_mode;       /* moe_a2a_mode (real ranks only; tp > 1 needs MOE_A2A_P2P):
                            * MOE_A2A_NCCL: count all-gather + one host sync to read the
                            *   G x E count matrix + grouped ncclSend/ncclRecv per (peer, expert);
                            * MOE_A2A_P2P: receive / expert-output buffers and a signal block
@@ -78,6 +88,8 @@ typedef struct {
                            *   hosting rank's receive rows) and the combine (NVLink loads of
                            *   the hosting rank's output rows) run inside the kernels with
                            *   epoch-valued release/acquire flags; no host synchronisation. */
+  int32_t tp;             /* tensor-parallel ranks per expert (0 or 1: none).  G % tp == 0,
+                           * tp <= 8, (F / tp) % 64 == 0; real ranks need MOE_A2A_P2P. */
 } moe_config;
 
 /* Host-side summary of the last dispatch (optional output of moe_dispatch). */
@@ -107,7 +119,7 @@ moe_status moe_ctx_sync(moe_ctx_t ctx);                   /* sync the last strea
 const char* moe_status_str(moe_status s);
 const char* moe_last_error(moe_ctx_t ctx);                /* "" if none; ctx may be NULL */
 int32_t moe_abi_version(void);                            /* MOE_ABI_VERSION */
-#define MOE_ABI_VERSION 1
+#define MOE_ABI_VERSION 2   /* 2: moe_config.tp */
 
 /* ---- a1: gating (G1, G2, G3) -------------------------------------
  * For each token t: idx[t][0..k-1] = the k largest logits[t][.] in descending
@@ -135,8 +147,9 @@ moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int
 
 /* ---- a3-a5: dispatch (G7, G8, G9, G13, G14) ---
  * x: bf16 [T][H] (this process's tokens); idx: int32 [T][k] from moe_route.
- * expert_to_rank: HOST int32 [E], values in [0, G) (the placement input; a rank
- * may host 0 experts).  Builds the stable send order (key P[e], e, t), the
+ * expert_to_rank: HOST int32 [E], values in [0, G/tp) (the placement input: the
+ * EP rank -- with tp > 1 the EP group -- hosting each expert; a rank may host 0
+ * experts).  Builds the stable send order (key P[e], e, t), the
  * expert-major receive layout (e ascending on g, then source s, then t; each
  * expert segment padded to the GEMM M tile) and moves every routed row to the rank
  * hosting its expert.  Collective when world > 1 (NCCL mode synchronises the
@@ -153,6 +166,11 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
  * with fp32 accumulation on tcgen05 tensor cores.  w13: bf16 packed
  * [n_w][2F][H] (see moe_pack_w13), w2: bf16 [n_w][H][F]; n_w experts in
  * ascending global id: the hosted experts (real mode) or all E (virtual).
+ * tp > 1, real ranks: this rank's slice q = rank % tp only, F_q = F / tp:
+ *   w13 = moe_pack_w13(W1[:, qF_q:(q+1)F_q, :], W3[same rows], n_w, F_q, H) [n_w][2F_q][H],
+ *   w2  = W2[:, :, qF_q:(q+1)F_q] made contiguous                          [n_w][H][F_q];
+ * Y is then this slice's bf16 partial output.  tp > 1, virtual ranks: the full
+ * w13 / w2 as above; every slice's partial output is computed separately. 
  * Collective in MOE_A2A_P2P mode: every rank calls it after moe_dispatch, also
  * a rank hosting no expert (w13/w2 may then be NULL) -- it raises the flag the
  * peers' moe_combine waits for. */
@@ -161,7 +179,8 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
 
 /* ---- a7-a8: combine (G4) -------------------------------------------------
  * Returns every expert output row to its source rank and writes
- * out[t] = bf16( sum_{j ascending} w[t][j] * Y[item (t,j)] ) in fp32.
+ * out[t] = bf16( sum_{j ascending} w[t][j] * Y[item (t,j)] ) in fp32; with
+ * tp > 1, Y[item] = sum_{q ascending} (partial output of TP slice q) in fp32.
  * w: float [T][k] (from moe_route); out: bf16 [T][H].  Uses the plan of the
  * last moe_dispatch (same T, k).  Collective when world > 1. */
 moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_t stream);
@@ -194,15 +213,16 @@ moe_status moe_layout_host(int32_t E, int32_t G, const int32_t* P, const int32_t
 
 /* Copies the plan of the last moe_dispatch to host arrays sized for the T and k
  * of that call (any pointer may be NULL):
- *   dest_rank [T][k]  rank hosting item (t, j)'s expert
+ *   dest_rank [T][k]  rank (EP group when tp > 1) hosting item (t, j)'s expert
  *   recv_pos  [T][k]  unpadded position of the item in that rank's receive order
  *   send_slot [T][k]  position of the item in its source's send order (C3 slot)
  *   cnt       [G][E]  count matrix of all ranks. */
 moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos,
                           int32_t* send_slot, int32_t* cnt);
 
-/* Expert FFN replaced by the identity (Y = received rows), for bit-exact
- * dispatch/combine tests (out must equal x). */
+/* Expert FFN replaced by the identity (Y = received rows; with tp > 1 TP slice 0
+ * returns the rows and the other slices zeros), for bit-exact dispatch/combine
+ * tests (out must equal x). */
 moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream);
 
 /* Copies the received rows of the last dispatch, in unpadded receive order of

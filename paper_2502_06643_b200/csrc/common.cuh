@@ -16,6 +16,7 @@ constexpr int kSegAlign = 128 * kGemmCG;  // receive-buffer expert segments are 
 constexpr int kMaxExperts = 256;
 constexpr int kMaxK = 16;
 constexpr int kMaxWorld = 64;
+constexpr int kMaxTP = 8;            // tensor-parallel ranks per EP group
 
 // Device error word bits (latched; surfaced by moe_ctx_sync as MOE_ERR_DEVICE).
 constexpr int kErrBadExpert = 1;
@@ -33,6 +34,10 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& v, float* f) {
+  f[0] = bf16_lo(v.x); f[1] = bf16_hi(v.x); f[2] = bf16_lo(v.y); f[3] = bf16_hi(v.y);
+  f[4] = bf16_lo(v.z); f[5] = bf16_hi(v.z); f[6] = bf16_lo(v.w); f[7] = bf16_hi(v.w);
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);   // RNE
   return *reinterpret_cast<uint32_t*>(&p);

@@ -212,10 +212,10 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
           rstart += pad_s[q];
           ++pos_r;
         }
-        if (!a.virt && !a.p2p && p_s[q] != a.me) send_base += ((volatile const int*)cnt)[a.me * E + q];
+        if (!a.virt && !a.p2p && p_s[q] != a.grp) send_base += ((volatile const int*)cnt)[a.me * E + q];
       }
     }
-    const bool hosted = a.virt || p == a.me;
+    const bool hosted = a.virt || p == a.grp;
     if (hosted) {
       const int pos = a.virt ? pos_v : pos_r;
       const long long start = a.virt ? vstart : rstart;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
   if (e == 0) {
     int n = 0, tp = 0, tu = 0;
     for (int q = 0; q < E; ++q)
-      if (a.virt || p_s[q] == a.me) {
+      if (a.virt || p_s[q] == a.grp) {
         ++n;
         tp += pad_s[q];
         tu += rows_s[q];
@@ -291,7 +291,7 @@ struct TileItems {
 __device__ __forceinline__ int item_slot(const PlanArgs& a, int p) {
   if (a.virt) return 0;
   if (a.p2p) return p;
-  return p == a.me ? 0 : 1;
+  return p == a.grp ? 0 : 1;
 }
 
 __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __restrict__ idx, const PlanBuffers& b,
@@ -363,10 +363,16 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
   const int nslots = a.p2p ? a.G : 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) dst_s[q] = b.dst_table[q];
   tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && mode != 2);
+  // P2P, tp > 1: slot p (an EP group) fans out to ranks p*tp .. p*tp+tp-1 (the TP
+  // all-gather inside the dispatch); otherwise a slot is one destination buffer
+  const bool fan = a.p2p && a.tp > 1;
   if (mode != 0) {  // drop the rows the other kernel copies
     const int n = (t1 - t0) * a.k;
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-      if (it.row[i] >= 0 && ((it.slot[i] == a.me) != (mode == 1))) it.row[i] = -1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (it.row[i] < 0) continue;
+      const bool drop = fan ? (mode == 1 && it.slot[i] != a.grp) : ((it.slot[i] == a.me) != (mode == 1));
+      if (drop) it.row[i] = -1;
+    }
     __syncthreads();
   }
   // copy: (token, 16-byte chunk) pairs, consecutive threads -> consecutive chunks
@@ -395,7 +401,16 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
         for (int j = 0; j < k; ++j) {
           const int i = tok * k + j;
           const int row = it.row[i];
-          if (row >= 0) dst_s[it.slot[i]][(long long)row * cpr + c] = v[u];
+          if (row < 0) continue;
+          if (!fan) {
+            dst_s[it.slot[i]][(long long)row * cpr + c] = v[u];
+          } else {
+            const int r0 = it.slot[i] * a.tp;
+            for (int q = 0; q < a.tp; ++q) {
+              const int r = r0 + q;
+              if (mode == 0 || ((r == a.me) == (mode == 1))) dst_s[r][(long long)row * cpr + c] = v[u];
+            }
+          }
         }
       }
     }
@@ -435,8 +450,13 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
   tile_info(a, blockIdx.x / a.col_split, s, t0, t1, tile0);
   const int k = KT > 0 ? KT : a.k;
   const int n = (t1 - t0) * k;
-  const int nslots = a.p2p ? a.G : 2;
-  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = a.fused ? b.ret_local : b.src_table[q];
+  // source of partial q of an item with slot sl: src_s[sl * tp + q].  P2P pull: the
+  // expert-output buffer of rank sl*tp+q; fused: the return buffer of slice q
+  // (slot 0); virtual: the expert-output buffer of slice q (slot 0); NCCL: slot.
+  const int nslots = (a.p2p && !a.fused) ? a.G : (a.tp > 1 ? a.tp : 2);
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x)
+    src_s[q] = a.fused ? b.ret_local + q * b.part_stride
+                       : ((a.virt && a.tp > 1) ? b.src_table[0] + q * b.part_stride : b.src_table[q]);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const long long gi = (long long)t0 * k + i;
     // fused combine: K6 already stored the row into this rank's return buffer at the C3 slot
@@ -452,6 +472,45 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
   const int c_lo = part * cw;
   const int width = max(0, min(cpr, c_lo + cw) - c_lo);
   const long long total = (long long)(t1 - t0) * width;
+  if (a.tp > 1) {
+    // Y[item] = sum_{q ascending} partial_q (fp32), then the j-ascending FMA of G4
+    for (long long p = threadIdx.x; p < total; p += blockDim.x) {
+      const int tok = (int)(p / width), c = c_lo + (int)(p % width);
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      for (int j = 0; j < k; ++j) {
+        const int i = tok * k + j;
+        const int row = row_s[i];
+        if (row < 0) continue;
+        const uint4* const* srcs = src_s + slot_s[i] * a.tp;
+        uint4 v[kMaxTP];
+#pragma unroll
+        for (int q = 0; q < kMaxTP; ++q)
+          if (q < a.tp) v[q] = __ldg(srcs[q] + (long long)row * cpr + c);
+        float y[8];
+        bf16x8_to_f32(v[0], y);
+#pragma unroll
+        for (int q = 1; q < kMaxTP; ++q)
+          if (q < a.tp) {
+            float z[8];
+            bf16x8_to_f32(v[q], z);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) y[e] += z[e];
+          }
+        const float wj = w_s[i];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaf(wj, y[e], acc[e]);
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      out[(long long)(t0 + tok) * cpr + c] = o;
+    }
+    return;
+  }
   constexpr int U = KT == 0 ? 1 : (KT <= 2 ? 4 : (KT <= 4 ? 2 : 1));
   constexpr int KL = KT == 0 ? 1 : KT;  // rows loaded per batch
   for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {

@@ -26,8 +26,10 @@ struct PlanArgs {
   int E;
   int H;
   int V;        // sources handled by this process (1 real, G virtual)
-  int G;        // EP group size
+  int G;        // ranks (sources): the EP group size, or EP groups x tp
   int me;       // real rank (0 in virtual mode)
+  int tp;       // tensor-parallel ranks per EP group (1: none); P[e] is an EP group id
+  int grp;      // this rank's EP group (me / tp)
   int virt;     // 1 = virtual ranks (every expert hosted by this process)
   int p2p;      // 1 = in-kernel NVLink peer stores/loads (real ranks)
   unsigned epoch;  // P2P flag value of this dispatch
@@ -60,6 +62,9 @@ struct PlanBuffers {
   int32_t* cslot_base;            // [E] send-order slot of this rank's first item for expert e
   int32_t* cslot_of_item;         // [T*k] send-order slot (C3) of every item of this rank
   const uint4* ret_local;         // this rank's return buffer
+  // tp > 1: the tp partial outputs of one item live part_stride uint4 apart (virtual
+  // mode: the expert-output buffers of the slices; fused combine: the return buffers)
+  long long part_stride;
 };
 
 // K5 per-tile arrival waits (P2P overlap): the producer waits only for the source
@@ -111,5 +116,8 @@ cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, i
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.
 bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// Same with a row pitch of ld elements (a column slice of a wider matrix).
+bool make_tmap_2d_ld(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                     uint32_t box_rows);
 
 }  // namespace moe

@@ -18,6 +18,10 @@ using namespace moe;
 struct moe_ctx {
   moe_config cfg{};
   int G = 1, V = 1, me = 0, virt = 0;
+  // tensor parallelism inside the experts (G20): EP group grp = me / tp, TP index
+  // tpi = me % tp; Fl = the FFN width this process computes per GEMM (F / tp for
+  // real TP ranks; F in virtual mode, whose K6 runs once per slice)
+  int tp = 1, grp = 0, tpi = 0, Fl = 0;
   int num_sms = 148;
   int E = 0, H = 0, F = 0;
   cudaStream_t last_stream = nullptr;
@@ -55,6 +59,8 @@ struct moe_ctx {
   alignas(64) uint8_t tmA2[128];  // A of GEMM2: hbuf [cap][F]
   alignas(64) uint8_t tmB1[128];
   alignas(64) uint8_t tmB2[128];
+  alignas(64) uint8_t tmA2s[kMaxTP][128];  // virtual TP: h column slice q
+  alignas(64) uint8_t tmB2s[kMaxTP][128];  // virtual TP: W2 column slice q
   const void* tmB1_ptr = nullptr;
   const void* tmB2_ptr = nullptr;
   int tmB_nw = -1;
@@ -150,6 +156,7 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.cslot_base = c->cslot_base;
   b.cslot_of_item = c->cslot_of_item;
   b.ret_local = reinterpret_cast<const uint4*>(c->retbuf);
+  b.part_stride = c->virt ? c->cap_rows * c->H / 8 : c->send_rows * c->H / 8;
   return b;
 }
 
@@ -162,6 +169,8 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.V = c->V;
   a.G = c->G;
   a.me = c->me;
+  a.tp = c->tp;
+  a.grp = c->grp;
   a.virt = c->virt;
   a.p2p = c->p2p;
   a.epoch = c->epoch;
@@ -286,6 +295,13 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   if (c.a2a_mode != MOE_A2A_NCCL && c.a2a_mode != MOE_A2A_P2P)
     return fail(ctx, MOE_ERR_INVALID_ARG, "unknown a2a_mode %d", c.a2a_mode);
   if (c.world > 1 && !uid) return fail(ctx, MOE_ERR_INVALID_ARG, "uid required when world > 1");
+  const int tp = c.tp <= 1 ? 1 : c.tp;
+  const int ranks = c.virtual_ranks > 1 ? c.virtual_ranks : c.world;
+  if (tp > kMaxTP) return fail(ctx, MOE_ERR_INVALID_ARG, "tp=%d > %d", tp, kMaxTP);
+  if (ranks % tp) return fail(ctx, MOE_ERR_INVALID_ARG, "tp=%d does not divide the %d ranks", tp, ranks);
+  if (c.ffn % (64 * tp)) return fail(ctx, MOE_ERR_UNSUPPORTED, "ffn / tp must be a multiple of 64");
+  if (tp > 1 && c.virtual_ranks <= 1 && c.a2a_mode != MOE_A2A_P2P)
+    return fail(ctx, MOE_ERR_UNSUPPORTED, "tp > 1 on real ranks needs MOE_A2A_P2P");
 
   ctx = new moe_ctx();
   ctx->cfg = c;
@@ -296,6 +312,10 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   ctx->G = ctx->virt ? c.virtual_ranks : c.world;
   ctx->V = ctx->virt ? c.virtual_ranks : 1;
   ctx->me = ctx->virt ? 0 : c.rank;
+  ctx->tp = tp;
+  ctx->grp = ctx->me / tp;
+  ctx->tpi = ctx->me % tp;
+  ctx->Fl = ctx->virt ? c.ffn : c.ffn / tp;
   auto bail = [&](moe_status s) {
     std::string m = ctx->err;
     moe_ctx_destroy(ctx);
@@ -349,10 +369,10 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->row_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
             A((void**)&ctx->err_dev, sizeof(int)) &&
             A((void**)&ctx->recv, (size_t)ctx->cap_rows * c.hidden * 2) &&
-            A((void**)&ctx->hbuf, (size_t)ctx->cap_rows * c.ffn * 2) &&
-            A((void**)&ctx->ybuf, (size_t)ctx->cap_rows * c.hidden * 2) &&
+            A((void**)&ctx->hbuf, (size_t)ctx->cap_rows * ctx->Fl * 2) &&
+            A((void**)&ctx->ybuf, (size_t)ctx->cap_rows * c.hidden * 2 * (ctx->virt ? tp : 1)) &&
             A((void**)&ctx->sendbuf, (size_t)ctx->send_rows * c.hidden * 2) &&
-            A((void**)&ctx->retbuf, (size_t)ctx->send_rows * c.hidden * 2) &&
+            A((void**)&ctx->retbuf, (size_t)ctx->send_rows * c.hidden * 2 * tp) &&
             A((void**)&ctx->slot_of_item, (size_t)std::max<int64_t>(Tm * k, 1)) &&
             A((void**)&ctx->dst_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
             A((void**)&ctx->src_table, sizeof(void*) * (size_t)std::max(G, 2)) &&
@@ -376,10 +396,17 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   ctx->cnt_host.assign((size_t)G * E, 0);
   // A-operand tensor maps over the context-owned activation buffers
   if (!make_tmap_2d(ctx->tmA1, ctx->recv, ctx->cap_rows, c.hidden, 128) ||
-      !make_tmap_2d(ctx->tmA2, ctx->hbuf, ctx->cap_rows, c.ffn, 128)) {
+      !make_tmap_2d(ctx->tmA2, ctx->hbuf, ctx->cap_rows, ctx->Fl, 128)) {
     fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
     return bail(MOE_ERR_CUDA);
   }
+  if (ctx->virt && tp > 1)
+    for (int q = 0; q < tp; ++q)
+      if (!make_tmap_2d_ld(ctx->tmA2s[q], ctx->hbuf + (size_t)q * (c.ffn / tp), ctx->cap_rows, c.ffn / tp, c.ffn,
+                           128)) {
+        fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for an h slice");
+        return bail(MOE_ERR_CUDA);
+      }
   if (!ctx->virt && G > 1) {
     ncclUniqueId id;
     memcpy(&id, uid, 128);
@@ -432,7 +459,7 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
           dst[g] = ctx->recv;
           src[g] = ctx->ybuf;
           sig[g] = ctx->sig;
-          ret[g] = ctx->retbuf;
+          ret[g] = ctx->retbuf + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
           continue;
         }
         const cudaIpcMemHandle_t* hg = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * g);
@@ -448,7 +475,8 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
         dst[g] = p[0];
         src[g] = p[1];
         sig[g] = p[2];
-        ret[g] = p[3];
+        // fused combine of TP slice tpi lands in partial region tpi of the source's buffer
+        ret[g] = static_cast<uint16_t*>(p[3]) + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
       }
     }
     if (cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -578,9 +606,10 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   if (!expert_to_rank) return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank is NULL");
   if (T > 0 && (!x || !idx)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
   const int E = ctx->E, G = ctx->G, H = ctx->H;
+  const int n_grp = G / ctx->tp;  // EP ranks (groups of tp ranks when tp > 1)
   for (int e = 0; e < E; ++e)
-    if (expert_to_rank[e] < 0 || expert_to_rank[e] >= G)
-      return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank[%d]=%d outside [0, %d)", e, expert_to_rank[e], G);
+    if (expert_to_rank[e] < 0 || expert_to_rank[e] >= n_grp)
+      return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank[%d]=%d outside [0, %d)", e, expert_to_rank[e], n_grp);
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   CU(cudaSetDevice(ctx->cfg.device));
@@ -592,7 +621,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     ctx->P_valid = true;
   }
   int n_hosted = 0;
-  for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->me);
+  for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->grp);
   ctx->n_hosted = n_hosted;
 
   if (ctx->p2p) {
@@ -666,16 +695,16 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     info->world = G;
     info->num_local_experts = n_hosted;
     int64_t rr = 0;
-    for (int g = 0; g < G && g < 64; ++g) {
+    for (int g = 0; g < n_grp && g < 64; ++g) {
       int64_t r = 0;
       for (int src = 0; src < G; ++src)
         for (int e = 0; e < E; ++e)
           if (expert_to_rank[e] == g) r += cnt[src * E + e];
       info->recv_counts[g] = (int32_t)r;
-      if (ctx->virt || g == ctx->me) rr += r;
+      if (ctx->virt || g == ctx->grp) rr += r;
     }
     if (!ctx->virt)
-      for (int g = 0; g < G && g < 64; ++g) {
+      for (int g = 0; g < n_grp && g < 64; ++g) {
         int64_t sc = 0;
         for (int e = 0; e < E; ++e)
           if (expert_to_rank[e] == g) sc += cnt[ctx->me * E + e];
@@ -700,7 +729,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // +1.5% at F = 14336 (Mixtral, 4EP; K6 loses two pipeline stages to the staging
   // buffer), profiles/r1_v8_*.  Default: on for F <= 8192; MOE_FUSED_COMBINE=0/1 overrides.
   {
-    bool fused = ctx->F <= 8192;
+    bool fused = ctx->Fl <= 8192;
     if (const char* env = getenv("MOE_FUSED_COMBINE")) fused = atoi(env) != 0;
     ctx->ffn_fused = ctx->p2p && fused;
   }
@@ -712,13 +741,18 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     return MOE_OK;
   }
   if (!w13 || !w2) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL weights");
-  const int H = ctx->H, F = ctx->F;
+  const int H = ctx->H, F = ctx->Fl, tp = ctx->tp;
+  const bool vslices = ctx->virt && tp > 1;  // virtual TP: K6 once per FFN slice
   const int nw_rows = ctx->virt ? ctx->E : nw;
   if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows) {
     const int bn1 = gemm_b_box_rows(2 * F, true, ctx->gemm_cg), bn2 = gemm_b_box_rows(H, false, ctx->gemm_cg);
     if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)nw_rows * 2 * F, H, bn1) ||
         !make_tmap_2d(ctx->tmB2, w2, (uint64_t)nw_rows * H, F, bn2))
       return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weights");
+    if (vslices)
+      for (int q = 0; q < tp; ++q)
+        if (!make_tmap_2d_ld(ctx->tmB2s[q], w2 + (size_t)q * (F / tp), (uint64_t)nw_rows * H, F / tp, F, bn2))
+          return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for a W2 slice");
     ctx->tmB1_ptr = w13;
     ctx->tmB2_ptr = w2;
     ctx->tmB_nw = nw_rows;
@@ -740,9 +774,21 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
                                       s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
-  e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
-                          ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s);
-  if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
+  if (!vslices) {
+    e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
+                            ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s);
+    if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
+  } else {
+    // partial output of FFN slice q (h columns and W2 columns [q F/tp, (q+1) F/tp))
+    // into expert-output buffer q; the combine sums the slices
+    for (int q = 0; q < tp; ++q) {
+      e = launch_grouped_gemm(ctx->tmA2s[q], ctx->tmB2s[q], ctx->ybuf + (size_t)q * ctx->cap_rows * H, H,
+                              ctx->seg_meta, ctx->E, H, F / tp, false, ctx->gemm_cg, ctx->num_sms, nowait,
+                              ctx->err_dev, ctx->done_counter + 2, plain, s);
+      if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 slice launch: %s", cudaGetErrorString(e));
+    }
+    ctx->launches += tp - 1;
+  }
   if (rec) {
     CU(cudaEventRecord(ev[2], s));
     ++ctx->timing_used;
@@ -793,7 +839,10 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
     launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, ctx->err_dev, s);
     LAUNCHED(ctx, 1);
   }
-  CU(cudaMemcpyAsync(ctx->ybuf, ctx->recv, (size_t)ctx->cap_rows * ctx->H * 2, cudaMemcpyDeviceToDevice, s));
+  const size_t ybytes = (size_t)ctx->cap_rows * ctx->H * 2;
+  if (ctx->tpi == 0) CU(cudaMemcpyAsync(ctx->ybuf, ctx->recv, ybytes, cudaMemcpyDeviceToDevice, s));
+  else CU(cudaMemsetAsync(ctx->ybuf, 0, ybytes, s));  // TP slices > 0 return zeros
+  if (ctx->virt && ctx->tp > 1) CU(cudaMemsetAsync(ctx->ybuf + ybytes / 2, 0, ybytes * (ctx->tp - 1), s));
   if (ctx->p2p) {
     launch_signal(a, b, 2, s);
     LAUNCHED(ctx, 1);
@@ -895,7 +944,7 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return P[x] < P[y]; });
     int64_t acc = 0;
     for (int e : order) {
-      if (!(ctx->virt || P[e] == ctx->me)) continue;
+      if (!(ctx->virt || P[e] == ctx->grp)) continue;
       int64_t r = 0;
       for (int s = 0; s < G; ++s) {
         pstart[(size_t)s * E + e] = acc + r;
@@ -910,7 +959,7 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
     int64_t acc = 0;
     for (int g = 0; g < G; ++g)
       for (int e = 0; e < E; ++e)
-        if (P[e] == g && !(ctx->virt || g == ctx->me)) {
+        if (P[e] == g && !(ctx->virt || g == ctx->grp)) {
           rbase[e] = acc;
           acc += cnt[(size_t)ctx->me * E + e];
         }
@@ -945,7 +994,7 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
             match = P[e] == slot;
             b0 = peer_base[(size_t)s * E + e];
           } else {
-            const bool remote = P[e] != ctx->me;
+            const bool remote = P[e] != ctx->grp;
             match = slot == (remote ? 1 : 0);
             b0 = remote ? rbase[e] : pstart[(size_t)s * E + e];
           }

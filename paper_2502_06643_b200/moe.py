@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmoe.so")
 
 MOE_OK = 0
+ABI_VERSION = 2  # include/moe.h MOE_ABI_VERSION (moe_config layout)
 STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_CUDA", 3: "MOE_ERR_NCCL", 4: "MOE_ERR_CAPACITY",
           5: "MOE_ERR_UNSUPPORTED", 6: "MOE_ERR_DEVICE", 7: "MOE_ERR_TIMEOUT"}
 
@@ -37,7 +38,7 @@ class Config(ctypes.Structure):
     _fields_ = [("max_tokens", ctypes.c_int32), ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
                 ("num_experts", ctypes.c_int32), ("max_k", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("device", ctypes.c_int32), ("virtual_ranks", ctypes.c_int32),
-                ("a2a_mode", ctypes.c_int32)]
+                ("a2a_mode", ctypes.c_int32), ("tp", ctypes.c_int32)]
 
 
 class DispatchInfo(ctypes.Structure):
@@ -80,6 +81,8 @@ def load_library(path=LIB_PATH):
     lib.moe_last_error.argtypes = [P]
     lib.moe_last_error.restype = ctypes.c_char_p
     lib.moe_abi_version.restype = ctypes.c_int32
+    if lib.moe_abi_version() != ABI_VERSION:
+        raise ImportError(f"{path}: ABI version {lib.moe_abi_version()} != {ABI_VERSION} (rebuild libmoe)")
     lib.moe_kernel_launches.argtypes = [P]
     lib.moe_kernel_launches.restype = ctypes.c_int64
     return lib
@@ -147,14 +150,28 @@ def pack_w13(w1, w3, stream=None):
     return w13
 
 
+def tp_slice_weights(w1, w3, w2, tp, q, stream=None):
+    """TP slice q of tp (moe.h, moe_expert_ffn): w1, w3 bf16 [n][F][H], w2 [n][H][F]
+    on the device -> (w13_q [n][2F/tp][H] packed, w2_q [n][H][F/tp] contiguous)."""
+    F = w1.shape[1]
+    f = F // tp
+    sl = slice(q * f, (q + 1) * f)
+    return (pack_w13(w1[:, sl].contiguous(), w3[:, sl].contiguous(), stream),
+            w2[:, :, sl].contiguous())
+
+
 class MoeLayer:
-    """One libmoe context (one EP rank, or G virtual ranks on one GPU)."""
+    """One libmoe context (one EP rank, or G virtual ranks on one GPU).
+
+    tp > 1: tensor parallelism inside the experts (moe.h; reading G20) -- the G
+    ranks form G/tp EP groups, the placement maps experts to groups."""
 
     def __init__(self, *, max_tokens, hidden, ffn, num_experts, max_k, world=1, rank=0, device=0,
-                 virtual_ranks=1, uid=None, a2a="nccl"):
+                 virtual_ranks=1, uid=None, a2a="nccl", tp=1):
         mode = {"nccl": 0, "p2p": 1}[a2a]
-        self.cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, world, rank, device, virtual_ranks, mode)
+        self.cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, world, rank, device, virtual_ranks, mode, tp)
         self.a2a = a2a
+        self.tp = tp
         self.E, self.H, self.F = num_experts, hidden, ffn
         self.G = virtual_ranks if virtual_ranks > 1 else world
         self.device = torch.device("cuda", device)

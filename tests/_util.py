@@ -74,3 +74,18 @@ class Inputs:
             w1, w3, w2 = cache[e]
             return ffn.swiglu(rows, w1, w3, w2)[1]
         return fn
+
+    def oracle_tp_fn(self, tp):
+        """expert_part_fn(e, rows, q) of oracle.layer.layer_ep_tp for these weights."""
+        from oracle import ffn
+        cache = {}
+
+        def fn(e, rows, q):
+            if e not in cache:
+                cache.clear()
+                cache[e] = tuple(bf16_to_f64(m) for m in self.w[e])
+            w1, w3, w2 = cache[e]
+            f = w1.shape[0] // tp
+            sl = slice(q * f, (q + 1) * f)
+            return ffn.swiglu(rows, w1[sl], w3[sl], w2[:, sl])[1]
+        return fn

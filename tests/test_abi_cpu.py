@@ -42,7 +42,7 @@ def test_every_declared_symbol_is_exported():
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(moe.EXPORTS) == decl
-    assert lib.moe_abi_version() == 1
+    assert lib.moe_abi_version() == 2
     assert lib.moe_status_str(4) == b"MOE_ERR_CAPACITY"
 
 
@@ -57,7 +57,9 @@ def test_contiguous_placement_and_error():
 def test_ctx_create_validates_before_touching_the_device():
     moe = _moe()
     bad = [dict(hidden=100), dict(ffn=0), dict(num_experts=0), dict(max_k=9), dict(world=2, rank=2),
-           dict(virtual_ranks=4, world=2)]
+           dict(virtual_ranks=4, world=2),
+           dict(virtual_ranks=6, tp=4), dict(virtual_ranks=4, tp=16), dict(virtual_ranks=4, tp=4, ffn=128),
+           dict(world=2, rank=0, tp=2)]   # tp: must divide the ranks, <= 8, F/tp % 64 == 0; real TP needs P2P
     for b in bad:
         kw = dict(max_tokens=16, hidden=64, ffn=128, num_experts=8, max_k=2, world=1, rank=0, device=0,
                   virtual_ranks=1)

@@ -42,3 +42,25 @@ def test_ep_over_real_ranks(n, a2a):
     assert p.returncode == 0, out[-4000:]
     for rank in range(n):
         assert f"RANK {rank} OK" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("n,tp,fused", [(2, 2, 0), (2, 2, 1), (4, 2, 0), (4, 2, 1), (4, 4, 1)])
+def test_tp_over_real_ranks(n, tp, fused):
+    """Tensor parallelism inside the experts (reading G20) over real ranks, P2P."""
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    port = 29900 + 10 * n + tp + fused + os.getpid() % 400
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_worker_tp.py")]
+    env = dict(os.environ, MOE_TEST_TP=str(tp), MOE_FUSED_COMBINE=str(fused))
+    p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, cwd=ROOT, env=env,
+                         start_new_session=True)
+    try:
+        out, _ = p.communicate(timeout=300)
+    except subprocess.TimeoutExpired:
+        os.killpg(p.pid, signal.SIGKILL)
+        out, _ = p.communicate()
+        pytest.fail("multi-GPU TP worker timed out:\n" + out[-4000:])
+    assert p.returncode == 0, out[-4000:]
+    for rank in range(n):
+        assert f"RANK {rank} OK" in out, out[-4000:]
