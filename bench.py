@@ -4,6 +4,7 @@ contiguous placement (BASELINE.json metric), through libmoe's C ABI.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config mixtral|tiny|e64] [--zipf-s S] [--placement contiguous|balanced|both]
+                    [--tp T] [--a2a p2p|nccl]
 
 A step is one pass of the whole hot path over one
 batch: moe_route -> moe_route_stats (layer l-1 -> l) -> moe_dispatch ->
@@ -11,7 +12,10 @@ moe_expert_ffn -> moe_combine.  Workload at every N: the Mixtral-8x7B MoE layer
 (E=8, top-2, H=4096, F=14336) over T = 16384 tokens in total (reading G15),
 Zipf-skewed router logits (s = 1.6, the paper's 64% layer-14 skew),
 synthetic bf16 data, random-init weights.  T is split across the N EP ranks
-(strong scaling); N = 1 hosts all 8 experts on one GPU.
+(strong scaling); N = 1 hosts all 8 experts on one GPU.  ``--tp t`` runs tensor
+parallelism inside the experts (N/t EP groups of t ranks, reading G20); the
+default is t = 2 for the Mixtral layer on 8 GPUs (BASELINE configs[3], the
+paper's 4EP-2TP) and t = 1 otherwise.
 
 Timing: W untimed warm-up steps, then K steps bracketed by a barrier and a
 device synchronize on both sides, CUDA events on the launching stream, max over
@@ -122,7 +126,9 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle (CPU) arm
-def oracle_expert_fn(weights64, weights_bf16):
+def oracle_expert_fn(weights64, weights_bf16, tp=1):
+    """expert_fn(e, rows) of oracle.layer.layer_ep, or (tp > 1) the TP slice
+    function expert_part_fn(e, rows, q) of oracle.layer.layer_ep_tp."""
     from oracle import ffn
     from oracle import bf16 as obf
 
@@ -131,16 +137,24 @@ def oracle_expert_fn(weights64, weights_bf16):
 
     cache = {}
 
-    def fn(e, rows):
+    def get(e):
         if weights64 is not None:
-            w1, w3, w2 = weights64[e]
-        else:
-            if e not in cache:
-                cache.clear()
-                cache[e] = tuple(to64(m) for m in weights_bf16[e])
-            w1, w3, w2 = cache[e]
+            return weights64[e]
+        if e not in cache:
+            cache.clear()
+            cache[e] = tuple(to64(m) for m in weights_bf16[e])
+        return cache[e]
+
+    def fn(e, rows):
+        w1, w3, w2 = get(e)
         return ffn.swiglu(rows, w1, w3, w2)[1]
-    return fn
+
+    def part(e, rows, q):
+        w1, w3, w2 = get(e)
+        f = w1.shape[0] // tp
+        sl = slice(q * f, (q + 1) * f)
+        return ffn.swiglu(rows, w1[sl], w3[sl], w2[:, sl])[1]
+    return fn if tp == 1 else part
 
 
 def oracle_setup(cfg, seed, s, G, P):
@@ -158,14 +172,15 @@ def oracle_setup(cfg, seed, s, G, P):
     return x, logits, wb, w64
 
 
-def oracle_time(cfg, n_tok, reps, seed, s, G, P, state=None):
-    """Time oracle.layer.layer_ep on `reps` samples of n_tok tokens of the workload."""
+def oracle_time(cfg, n_tok, reps, seed, s, G, P, state=None, tp=1):
+    """Time oracle.layer.layer_ep (layer_ep_tp when tp > 1) on `reps` samples of
+    n_tok tokens of the workload."""
     from oracle import layer as olayer
     from oracle import bf16 as obf
     if state is None:
         state = oracle_setup(cfg, seed, s, G, P)
     x, logits, wb, w64 = state
-    fn = oracle_expert_fn(w64, wb)
+    fn = oracle_expert_fn(w64, wb, tp)
     rng = np.random.default_rng(seed + 99)
     times = []
     for _ in range(reps):
@@ -173,7 +188,10 @@ def oracle_time(cfg, n_tok, reps, seed, s, G, P, state=None):
         xs = obf.from_bits(x[sel].contiguous().view(torch.int16).numpy().view(np.uint16))
         ls = logits[sel].numpy()
         t0 = time.perf_counter()
-        olayer.layer_ep(xs, ls, cfg["k"], np.asarray(P), G, fn)
+        if tp == 1:
+            olayer.layer_ep(xs, ls, cfg["k"], np.asarray(P), G, fn)
+        else:
+            olayer.layer_ep_tp(xs, ls, cfg["k"], np.asarray(P), G, tp, fn)
         times.append(time.perf_counter() - t0)
     return times, state
 
@@ -473,7 +491,12 @@ def run_ours(args):
         r = results[head]
         R = r["rows_rank0"]
         flops_k5 = 4.0 * H * Fl * R
-        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+        # the sustained (power-capped) cuBLAS figure when the SM clock sagged under the
+        # load (the usual case for this long step), the burst figure when it held max
+        clk = r["clocks"] or {}
+        capped = not clk.get("sm_mhz") or not clk.get("sm_max_mhz") or clk["sm_mhz"] < 0.97 * clk["sm_max_mhz"]
+        peak_kind = "sustained" if capped else "burst"
+        peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) if capped else peaks.get("bf16_tflops")
         ach = flops_k5 / (r["k5_ms"] * 1e-3) / 1e12 if r["k5_ms"] else None
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -497,7 +520,8 @@ def run_ours(args):
                          "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                          "frac": (ach / peak) if ach else None, "traffic": traffic,
                          "flops_per_launch": flops_k5, "launch_ms": r["k5_ms"],
-                         "peak_source": peaks_src + " bf16 sustained (kernel timed inside a long step)",
+                         "peak_source": peaks_src + (" bf16 sustained (SM clock below max under this load)" if capped
+                                                     else " bf16 burst (SM clock held its max during the run)"),
                          "frac_of_burst": (ach / peaks.get("bf16_tflops")) if ach else None,
                          "k6_ms": r["k6_ms"],
                          "k6_frac": (2.0 * H * Fl * R / (r["k6_ms"] * 1e-3) / 1e12 / peak) if r["k6_ms"] else None},
@@ -531,12 +555,15 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     N = args.gpus
     E = cfg["E"]
-    P = np.array([e // (E // N) for e in range(E)], dtype=np.int32) if E % N == 0 else np.zeros(E, np.int32)
-    G = N if E % N == 0 else 1
+    tp = args.tp
+    G = N // tp if E % (N // tp) == 0 else 1
+    if G == 1:
+        tp = 1
+    P = np.array([e // (E // G) for e in range(E)], dtype=np.int32)
     state = oracle_setup(cfg, args.seed, args.zipf_s, G, P)
     if args.warmup:
-        oracle_time(cfg, args.ref_tokens, min(args.warmup, 3), args.seed, args.zipf_s, G, P, state)
-    times, _ = oracle_time(cfg, args.ref_tokens, args.steps, args.seed + 1, args.zipf_s, G, P, state)
+        oracle_time(cfg, args.ref_tokens, min(args.warmup, 3), args.seed, args.zipf_s, G, P, state, tp)
+    times, _ = oracle_time(cfg, args.ref_tokens, args.steps, args.seed + 1, args.zipf_s, G, P, state, tp)
     total = sum(times)
     val = args.ref_tokens * len(times) / total
     ms = total / len(times) * 1e3
@@ -544,11 +571,12 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"], "experts": E, "top_k": cfg["k"], "hidden": cfg["H"],
-                       "ffn": cfg["F"], "tokens_total": cfg["T"], "ep": G, "placement": "contiguous",
+                       "ffn": cfg["F"], "tokens_total": cfg["T"], "ep": G, "tp": tp, "placement": "contiguous",
                        "zipf_s": args.zipf_s},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads_used(), "kind": "oracle",
                              "sample": f"each step = {args.ref_tokens} random tokens of the workload through "
-                                       f"oracle.layer.layer_ep (float64 numpy) on the host cores"},
+                                       f"oracle.layer.layer_ep{'_tp' if tp > 1 else ''} (float64 numpy) on the host "
+                                       f"cores"},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     del world
@@ -566,13 +594,16 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--a2a", choices=["nccl", "p2p"], default="p2p",
                     help="all-to-all transport between real ranks (N > 1)")
-    ap.add_argument("--tp", type=int, default=1,
-                    help="tensor-parallel ranks per expert (EP groups = gpus / tp; reading G20)")
+    ap.add_argument("--tp", type=int, default=None,
+                    help="tensor-parallel ranks per expert (EP groups = gpus / tp; reading G20); default 2 for "
+                         "the Mixtral layer on 8 GPUs (BASELINE configs[3]: 4EP-2TP on 8 B200), else 1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=2048)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=32)
     args = ap.parse_args()
+    if args.tp is None:
+        args.tp = 2 if (args.gpus == 8 and args.config == "mixtral") else 1
     if args.warmup < 3 and args.impl == "ours":
         raise SystemExit("--warmup must be >= 3")
     if args.impl == "reference":
