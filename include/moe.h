@@ -243,6 +243,18 @@ int64_t moe_kernel_launches(moe_ctx_t ctx);
 moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t max_records);
 moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms, int32_t max_records, int32_t* n_out);
 
+/* Layer timeline (profiling).  moe_timeline_enable(ctx, n) arms n records (0
+ * disarms); each of the next n moe_dispatch -> moe_expert_ffn -> moe_combine
+ * sequences records 8 CUDA events: 0 dispatch entry, 1 after the plan/layout
+ * kernels (P2P: includes the count all-gather), 2 after the scatter on `stream`
+ * (P2P: this rank's own rows), 3 after the scatter of the peers' rows (P2P side
+ * stream; else = 2), 4 expert_ffn entry, 5 after K5, 6 after K6, 7 after the
+ * combine kernel.  moe_timeline_read synchronises the device and writes
+ * ms[i][j] = event j - event 0 of record i in milliseconds (host float
+ * [max_records][8]; -1 for an event that was not recorded), then re-arms. */
+moe_status moe_timeline_enable(moe_ctx_t ctx, int32_t max_records);
+moe_status moe_timeline_read(moe_ctx_t ctx, float* ms, int32_t max_records, int32_t* n_out);
+
 #ifdef __cplusplus
 }
 #endif

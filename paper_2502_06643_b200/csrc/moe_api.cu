@@ -68,6 +68,10 @@ struct moe_ctx {
   // optional K5/K6 timing event records (3 events per moe_expert_ffn call)
   std::vector<cudaEvent_t> ev;
   int timing_used = 0;
+  // optional layer timeline: kTimeline events per dispatch -> expert_ffn -> combine
+  std::vector<cudaEvent_t> tl;
+  std::vector<uint8_t> tl_mask;  // [record] bit j = event j recorded
+  int tl_used = 0, tl_cur = -1;
 
   // per-item destination slot, pointer tables (slot -> buffer), P2P state
   uint8_t* slot_of_item = nullptr;
@@ -94,6 +98,7 @@ struct moe_ctx {
   // P2P overlap: rows for peers are pushed on a side stream while K5 starts on
   // this rank's own rows (fork after the layout kernel, join in combine)
   cudaStream_t side = nullptr;
+  bool local_first = false;             // MOE_SCATTER_LOCAL_FIRST: own rows launched before the fork
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // last dispatch
@@ -132,6 +137,12 @@ static moe_status fail(moe_ctx_t c, moe_status s, const char* fmt, ...) {
     if (e_ != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "kernel launch: %s", cudaGetErrorString(e_)); \
     (ctx)->launches += (n);                                                               \
   } while (0)
+
+static constexpr int kTimeline = 8;
+static void tl_rec(moe_ctx_t c, int j, cudaStream_t s) {
+  if (c->tl_cur < 0) return;
+  if (cudaEventRecord(c->tl[(size_t)c->tl_cur * kTimeline + j], s) == cudaSuccess) c->tl_mask[c->tl_cur] |= 1u << j;
+}
 
 static PlanBuffers plan_buffers(moe_ctx_t c) {
   PlanBuffers b;
@@ -430,7 +441,12 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     sig[0] = ctx->sig;
     if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
       ctx->p2p = true;
-      if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+      int prio_lo = 0, prio_hi = 0;
+      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+      const char* sp = getenv("MOE_SIDE_PRIORITY");  // "high": the peers' rows get SMs first
+      const int prio = (sp && !strcmp(sp, "high")) ? prio_hi : prio_lo;
+      ctx->local_first = getenv("MOE_SCATTER_LOCAL_FIRST") && atoi(getenv("MOE_SCATTER_LOCAL_FIRST")) != 0;
+      if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         fail(ctx, MOE_ERR_CUDA, "side stream / event creation failed");
@@ -514,6 +530,8 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->tl)
     if (e) cudaEventDestroy(e);
   if (ctx->P_pinned) cudaFreeHost(ctx->P_pinned);
   if (ctx->cnt_pinned) cudaFreeHost(ctx->cnt_pinned);
@@ -624,6 +642,9 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->grp);
   ctx->n_hosted = n_hosted;
 
+  ctx->tl_cur = ctx->tl_used < (int)ctx->tl_mask.size() ? ctx->tl_used : -1;
+  if (ctx->tl_cur >= 0) ctx->tl_mask[ctx->tl_cur] = 0;
+  tl_rec(ctx, 0, s);
   if (ctx->p2p) {
     ++ctx->epoch;
     // the previous layer's side-stream scatter reads plan arrays this call rewrites
@@ -642,17 +663,27 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     memcpy(ctx->cnt_host.data(), ctx->cnt_pinned, sizeof(int32_t) * G * E);
   }
   launch_layout(a, b, ctx->cap_rows, s);  // P2P: also the in-kernel count all-gather
+  tl_rec(ctx, 1, s);
   if (ctx->p2p) {
     // rows for peers: NVLink stores on the side stream (arrival flags raised by its
     // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
+    if (ctx->local_first) {
+      launch_scatter(a, x, idx, b, 1, s);
+      tl_rec(ctx, 2, s);
+    }
     CU(cudaEventRecord(ctx->ev_fork, s));
     CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     launch_scatter(a, x, idx, b, 2, ctx->side);
+    tl_rec(ctx, 3, ctx->side);
     CU(cudaEventRecord(ctx->ev_join, ctx->side));
-    launch_scatter(a, x, idx, b, 1, s);
+    if (!ctx->local_first) {
+      launch_scatter(a, x, idx, b, 1, s);
+      tl_rec(ctx, 2, s);
+    }
     LAUNCHED(ctx, 3);
   } else {
     launch_scatter(a, x, idx, b, 0, s);
+    tl_rec(ctx, 2, s);
     LAUNCHED(ctx, 2);
   }
   if (nccl) {
@@ -757,6 +788,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     ctx->tmB2_ptr = w2;
     ctx->tmB_nw = nw_rows;
   }
+  tl_rec(ctx, 4, s);
   const bool rec = ctx->timing_used < (int)ctx->ev.size() / 3;
   cudaEvent_t* ev = rec ? &ctx->ev[3 * ctx->timing_used] : nullptr;
   if (rec) CU(cudaEventRecord(ev[0], s));
@@ -774,6 +806,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
                                       s);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
+  tl_rec(ctx, 5, s);
   if (!vslices) {
     e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
                             ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s);
@@ -793,6 +826,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     CU(cudaEventRecord(ev[2], s));
     ++ctx->timing_used;
   }
+  tl_rec(ctx, 6, s);
   ctx->launches += 2;
   if (ctx->p2p) {  // expert outputs of this rank are ready for the peers' combine
     launch_signal(a, b, 2, s);
@@ -822,6 +856,36 @@ moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms, int32_t max_records, in
   }
   *n_out = n;
   ctx->timing_used = 0;
+  return MOE_OK;
+}
+
+moe_status moe_timeline_enable(moe_ctx_t ctx, int32_t max_records) {
+  if (!ctx || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaDeviceSynchronize());
+  for (auto& e : ctx->tl) cudaEventDestroy(e);
+  ctx->tl.assign((size_t)kTimeline * max_records, nullptr);
+  for (auto& e : ctx->tl) CU(cudaEventCreate(&e));
+  ctx->tl_mask.assign(max_records, 0);
+  ctx->tl_used = 0;
+  ctx->tl_cur = -1;
+  return MOE_OK;
+}
+
+moe_status moe_timeline_read(moe_ctx_t ctx, float* ms, int32_t max_records, int32_t* n_out) {
+  if (!ctx || !ms || !n_out || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaDeviceSynchronize());
+  const int n = std::min(ctx->tl_used, max_records);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < kTimeline; ++j) {
+      float v = -1.f;
+      if ((ctx->tl_mask[i] & 1u) && (ctx->tl_mask[i] >> j & 1u))
+        CU(cudaEventElapsedTime(&v, ctx->tl[(size_t)i * kTimeline], ctx->tl[(size_t)i * kTimeline + j]));
+      ms[(size_t)i * kTimeline + j] = v;
+    }
+  *n_out = n;
+  ctx->tl_used = 0;
   return MOE_OK;
 }
 
@@ -888,6 +952,11 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   PlanBuffers b = plan_buffers(ctx);
   launch_combine(a, w, b, out, s);
   LAUNCHED(ctx, a.n_tiles > 0);
+  tl_rec(ctx, 7, s);
+  if (ctx->tl_cur >= 0) {
+    ++ctx->tl_used;
+    ctx->tl_cur = -1;
+  }
   if (ctx->p2p) CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));  // join the side stream
   return MOE_OK;
 }

@@ -25,7 +25,7 @@ EXPORTS = ["moe_get_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_sy
            "moe_last_error", "moe_abi_version", "moe_route", "moe_route_stats", "moe_stats_allreduce",
            "moe_dispatch", "moe_expert_ffn", "moe_combine", "moe_pack_w13", "moe_placement_contiguous",
            "moe_layout_host", "moe_debug_plan", "moe_debug_identity_ffn", "moe_debug_recv", "moe_kernel_launches",
-           "moe_ffn_timing_enable", "moe_ffn_timing_read"]
+           "moe_ffn_timing_enable", "moe_ffn_timing_read", "moe_timeline_enable", "moe_timeline_read"]
 
 
 class MoeError(RuntimeError):
@@ -71,6 +71,8 @@ def load_library(path=LIB_PATH):
         "moe_debug_recv": [P, P, I64, P],
         "moe_ffn_timing_enable": [P, I32],
         "moe_ffn_timing_read": [P, P, I32, P],
+        "moe_timeline_enable": [P, I32],
+        "moe_timeline_read": [P, P, I32, P],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -213,6 +215,21 @@ class MoeLayer:
         got = ctypes.c_int32()
         self._c(_lib.moe_ffn_timing_read(self._ctx, ms, n, ctypes.byref(got)))
         return [(float(ms[2 * i]), float(ms[2 * i + 1])) for i in range(got.value)]
+
+    TIMELINE = ("dispatch", "layout", "scatter_local", "scatter_peers", "ffn", "k5", "k6", "combine")
+
+    def timeline(self, max_records):
+        """Arm the 8-event layer timeline for the next max_records layers (moe.h)."""
+        self._c(_lib.moe_timeline_enable(self._ctx, int(max_records)))
+        self._tl_max = int(max_records)
+
+    def timeline_read(self):
+        """[[ms of each TIMELINE event after dispatch entry] per recorded layer]."""
+        n = getattr(self, "_tl_max", 0)
+        ms = (ctypes.c_float * (8 * max(n, 1)))()
+        got = ctypes.c_int32()
+        self._c(_lib.moe_timeline_read(self._ctx, ms, n, ctypes.byref(got)))
+        return [[float(ms[8 * i + j]) for j in range(8)] for i in range(got.value)]
 
     def sync(self):
         self._c(_lib.moe_ctx_sync(self._ctx))
