@@ -45,9 +45,11 @@ struct GemmCfg {
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // fused-combine epilogue: each epilogue warp stages its 32 output rows (bf16) so
-  // that remote NVLink stores are whole rows written by the 32 lanes together
-  static constexpr int STAGING = FUSED ? 4 * 32 * BN * 2 : 0;
+  // fused-combine epilogue: each epilogue warp stages its 32 output rows (bf16,
+  // row pitch padded by 16 bytes so the lane-per-row writes are conflict-free);
+  // each row then leaves as one bulk async copy (TMA engine) to its destination
+  static constexpr int STAGE_PITCH = BN * 2 + 16;
+  static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 0;
   static constexpr int BUDGET = kSmemBudget - STAGING;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
@@ -417,8 +419,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // NVLink.  The warp stages its 32 rows in shared memory (16-byte granules,
         // XOR-swizzled by row), releases the accumulator, then writes row by row with
         // all 32 lanes so every NVLink store is a whole contiguous row segment.
-        constexpr int GR = BN / 8;  // 16-byte granules per row
-        uint4* stg = reinterpret_cast<uint4*>(staging) + (size_t)(warp - 2) * 32 * GR;
+        constexpr int PITCH = C::STAGE_PITCH;
+        uint8_t* stg = staging + (size_t)(warp - 2) * 32 * PITCH;
+        uint8_t* my_row = stg + (size_t)lane * PITCH;
         unsigned long long dst_row = 0;
         const int32_t* ss = fr.seg_src + (long long)seg * fr.G * 3;
         for (int s = 0; s < fr.G; ++s) {
@@ -429,20 +432,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             break;
           }
         }
+        bulk_wait_read_all();  // this lane's previous row copy has left the staging row
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int g = c / 8 + i;
-            stg[lane * GR + (g ^ (lane & (GR - 1)))] =
+          for (int i = 0; i < 4; ++i)
+            reinterpret_cast<uint4*>(my_row)[c / 8 + i] =
                 make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]), __uint_as_float(v[8 * i + 1])),
                            pack_bf16x2(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
                            pack_bf16x2(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
                            pack_bf16x2(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
-          }
         }
         tc_fence_before();
         __syncwarp();
@@ -450,14 +452,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
           else mbar_arrive(&tempty[acc]);
         }
-#pragma unroll 1
-        for (int r = 0; r < 32; ++r) {
-          const unsigned long long p = __shfl_sync(0xffffffffu, dst_row, r);
-          if (p == 0) continue;  // padding row
-          uint4* dst = reinterpret_cast<uint4*>(p);
-          for (int g = lane; g < GR; g += 32) dst[g] = stg[r * GR + (g ^ (r & (GR - 1)))];
+        // every lane ships its own row (a contiguous BN-column segment of the
+        // destination row) with one bulk copy; the copy engine keeps the NVLink
+        // stores in flight while the warp moves on to the next accumulator
+        fence_proxy_async_smem();
+        if (dst_row != 0) {
+          bulk_s2g(reinterpret_cast<void*>(dst_row), smem_u32(my_row), BN * 2);
+          bulk_commit();
         }
-        __syncwarp();
       } else {
         uint16_t* drow = D + grow * ldd + (long long)nt * BN;
 #pragma unroll 1
@@ -487,7 +489,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         acc_phase ^= 1;
       }
     }
-    if constexpr (FUSED) __threadfence_system();  // peer stores visible before the ready flag
+    if constexpr (FUSED) {  // peer stores complete and visible before the ready flag
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence_system();
+    }
   }
 
   tc_fence_before();
