@@ -17,6 +17,7 @@ constexpr int kMaxExperts = 256;
 constexpr int kMaxK = 16;
 constexpr int kMaxWorld = 64;
 constexpr int kMaxTP = 8;            // tensor-parallel ranks per EP group
+constexpr int kPushChunk = 32;       // rows per k_push work unit (one expert's send-order run)
 
 // Device error word bits (latched; surfaced by moe_ctx_sync as MOE_ERR_DEVICE).
 constexpr int kErrBadExpert = 1;

@@ -260,6 +260,45 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
       }
     }
   }
+  if (a.p2p) {
+    // slot-ordered push work table (k_push): one item per expert with rows for peers,
+    // ordered by (position of e among its group's experts, destination group rotated
+    // so that rank me starts with group grp+1): every destination receives its first
+    // experts from every source early, and no two sources start on the same target
+    const int n_grp = a.G / a.tp;
+    __shared__ int key_s[kMaxExperts], chunks_s[kMaxExperts], pos_s[kMaxExperts];
+    if (e < E) {
+      const int p = p_s[e];
+      int pos = 0;
+      for (int q = 0; q < e; ++q) pos += (p_s[q] == p);
+      const bool incl = (p != a.grp || a.tp > 1) && b.cnt_local[e] > 0;
+      key_s[e] = incl ? pos * n_grp + (p - a.grp - 1 + 2 * n_grp) % n_grp : -1;
+      chunks_s[e] = incl ? (b.cnt_local[e] + kPushChunk - 1) / kPushChunk : 0;
+      pos_s[e] = pos;
+    }
+    __syncthreads();
+    if (e < E && key_s[e] >= 0) {
+      int rank = 0, first = 0;
+      for (int q = 0; q < E; ++q)
+        if (key_s[q] >= 0 && key_s[q] < key_s[e]) {
+          ++rank;
+          first += chunks_s[q];
+        }
+      b.push_work[2 + 3 * rank] = e;
+      b.push_work[3 + 3 * rank] = first;
+      b.push_work[4 + 3 * rank] = pos_s[e];
+    }
+    if (e == 0) {
+      int items = 0, chunks = 0;
+      for (int q = 0; q < E; ++q)
+        if (key_s[q] >= 0) {
+          ++items;
+          chunks += chunks_s[q];
+        }
+      b.push_work[0] = items;
+      b.push_work[1] = chunks;
+    }
+  }
   if (e == 0) {
     int n = 0, tp = 0, tu = 0;
     for (int q = 0; q < E; ++q)
@@ -330,7 +369,10 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
       if (write_plan) {
         b.row_of_item[(long long)t0 * a.k + i] = row;
         b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
-        if (a.p2p) b.cslot_of_item[(long long)t0 * a.k + i] = cslot;
+        if (a.p2p) {
+          b.cslot_of_item[(long long)t0 * a.k + i] = cslot;
+          if (cslot >= 0) b.item_of_slot[cslot] = t0 * a.k + i;
+        }
       }
     }
     __syncthreads();
@@ -356,21 +398,24 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
   __shared__ unsigned last;
   // col_split CTAs share a token tile; each recomputes the (cheap) in-tile
   // ranks and copies one slice of the hidden dimension
-  const int part = blockIdx.x % a.col_split;
-  const int tile = blockIdx.x / a.col_split;
+  const int split = mode == 3 ? 1 : a.col_split;  // mode 3 copies nothing: one CTA per tile
+  const int part = blockIdx.x % split;
+  const int tile = blockIdx.x / split;
   int s, t0, t1, tile0;
   tile_info(a, tile, s, t0, t1, tile0);
   const int nslots = a.p2p ? a.G : 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) dst_s[q] = b.dst_table[q];
-  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && mode != 2);
+  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && (mode == 0 || mode == 1 || mode == 3));
+  if (mode == 3) return;
   // P2P, tp > 1: slot p (an EP group) fans out to ranks p*tp .. p*tp+tp-1 (the TP
   // all-gather inside the dispatch); otherwise a slot is one destination buffer
   const bool fan = a.p2p && a.tp > 1;
+  const bool local_only = mode == 1 || mode == 4;
   if (mode != 0) {  // drop the rows the other kernel copies
     const int n = (t1 - t0) * a.k;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       if (it.row[i] < 0) continue;
-      const bool drop = fan ? (mode == 1 && it.slot[i] != a.grp) : ((it.slot[i] == a.me) != (mode == 1));
+      const bool drop = fan ? (local_only && it.slot[i] != a.grp) : ((it.slot[i] == a.me) != local_only);
       if (drop) it.row[i] = -1;
     }
     __syncthreads();
@@ -408,14 +453,14 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
             const int r0 = it.slot[i] * a.tp;
             for (int q = 0; q < a.tp; ++q) {
               const int r = r0 + q;
-              if (mode == 0 || ((r == a.me) == (mode == 1))) dst_s[r][(long long)row * cpr + c] = v[u];
+              if (mode == 0 || ((r == a.me) == local_only)) dst_s[r][(long long)row * cpr + c] = v[u];
             }
           }
         }
       }
     }
   }
-  if (a.p2p && mode != 1) {
+  if (a.p2p && (mode == 0 || mode == 2)) {
     // the last CTA to finish raises flag_data[me] on every rank
     __threadfence_system();
     __syncthreads();
@@ -425,6 +470,88 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
       *b.done_counter = 0;
       signal_all(a, b, 1);
     }
+  }
+}
+
+// ----------------------------------------------------------------- K4: slot-ordered P2P push
+// Rows for peers in this rank's send order (C3 slots), chunk by chunk (kPushChunk
+// rows of one expert); chunk order follows k_layout's work table.  Each chunk
+// gathers its token rows of x (16-byte vectors) and stores them into the
+// destination rows of every target rank (the tp ranks of the expert's group,
+// except this rank).  When an expert's last chunk lands, flag_seg[me][pos] is
+// released on the targets, so their K5 starts on that expert's rows while the
+// rest is still in flight; the last CTA also raises flag_data (whole source).
+__global__ void __launch_bounds__(kScatterThreads) k_push(PlanArgs a, const uint4* __restrict__ x, PlanBuffers b) {
+  __shared__ int tok_s[kPushChunk];
+  __shared__ uint4* dst_s[kMaxTP];
+  __shared__ int info_s[4];
+  __shared__ unsigned last;
+  const int items = b.push_work[0], chunks = b.push_work[1];
+  const int cpr = a.H / 8;
+  for (int c = blockIdx.x; c < chunks; c += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int lo = 0, hi = items - 1;  // last item whose first chunk <= c
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) / 2;
+        if (b.push_work[3 + 3 * mid] <= c) lo = mid;
+        else hi = mid - 1;
+      }
+      const int e = b.push_work[2 + 3 * lo];
+      const int r0 = (c - b.push_work[3 + 3 * lo]) * kPushChunk;
+      info_s[0] = e;
+      info_s[1] = r0;
+      info_s[2] = min(kPushChunk, b.cnt_local[e] - r0);
+      info_s[3] = b.push_work[4 + 3 * lo];
+    }
+    __syncthreads();
+    const int e = info_s[0], r0 = info_s[1], n = info_s[2];
+    const int p = b.P[e];
+    int nt = 0;
+    if (threadIdx.x == 0)
+      for (int q = 0; q < a.tp; ++q)
+        if (p * a.tp + q != a.me) dst_s[nt++] = b.dst_table[p * a.tp + q];
+    nt = a.tp - (p == a.grp ? 1 : 0);
+    const int cs = b.cslot_base[e] + r0;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) tok_s[r] = b.item_of_slot[cs + r] / a.k;
+    __syncthreads();
+    const long long drow0 = (long long)b.base_row[e] + r0;
+    const int total = n * cpr;
+    constexpr int U = 4;
+    for (int p0 = threadIdx.x; p0 < total; p0 += blockDim.x * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = p0 + u * blockDim.x;
+        if (q < total) v[u] = __ldg(x + (long long)tok_s[q / cpr] * cpr + q % cpr);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = p0 + u * blockDim.x;
+        if (q < total)
+          for (int d = 0; d < nt; ++d) dst_s[d][(drow0 + q / cpr) * cpr + q % cpr] = v[u];
+      }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(&b.done_rows[e], n);
+      if (old + n == b.cnt_local[e]) {  // this expert's rows have all landed
+        b.done_rows[e] = 0;
+        __threadfence_system();
+        for (int q = 0; q < a.tp; ++q)
+          if (p * a.tp + q != a.me) st_release_sys(&b.peer_sig[p * a.tp + q]->flag_seg[a.me][info_s[3]], a.epoch);
+      }
+    }
+    __syncthreads();
+  }
+  // the last CTA raises flag_data[me] on every rank (combine / identity paths)
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(b.done_counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    *b.done_counter = 0;
+    signal_all(a, b, 1);
   }
 }
 
@@ -603,9 +730,14 @@ void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, co
                     cudaStream_t s) {
   const size_t smem = sizeof(int) * (kScatterThreads / 32) * a.E;
   if (a.n_tiles > 0)
-    k_scatter<<<a.n_tiles * a.col_split, kScatterThreads, smem, s>>>(a, (const uint4*)x, idx, b, mode);
-  else if (a.p2p && mode != 1)
+    k_scatter<<<a.n_tiles * (mode == 3 ? 1 : a.col_split), kScatterThreads, smem, s>>>(a, (const uint4*)x, idx,
+                                                                                       b, mode);
+  else if (a.p2p && (mode == 0 || mode == 2))
     k_signal<<<1, 32, 0, s>>>(a, b, 1);
+}
+void launch_push(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int num_sms, cudaStream_t s) {
+  // enough CTAs to keep NVLink busy, few enough to co-reside with K5 (one per SM)
+  k_push<<<num_sms, kScatterThreads, 0, s>>>(a, (const uint4*)x, b);
 }
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
   k_signal<<<1, 32, 0, s>>>(a, b, which);

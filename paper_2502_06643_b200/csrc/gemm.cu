@@ -36,8 +36,7 @@ namespace moe {
 
 constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kGemmThreads = 192;
-constexpr int kSmemBudget = 200 * 1024;       // leaves room for a co-resident k_scatter CTA (P2P overlap)
-constexpr int kSmemBudgetFused = 212 * 1024;  // K6 fused combine runs alone
+constexpr int kSmemBudget = 200 * 1024;
 constexpr int kSchedRing = 8;  // depth of the tile-scheduler ring
 
 template <int BN, int CG, bool FUSED = false>
@@ -46,14 +45,12 @@ struct GemmCfg {
   static constexpr int B_ROWS = BN / CG;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // fused-combine epilogue: each epilogue warp stages 32 rows x 32 columns (bf16,
-  // row pitch 80 bytes so the lane-per-row writes are conflict-free) in one of two
-  // buffers; each lane's 64-byte row piece leaves as a bulk async copy (TMA engine)
-  // to its destination, so the staging area stays small and K6 keeps its stages
-  static constexpr int STAGE_PITCH = 80;
-  static constexpr int STAGE_BUF = 32 * STAGE_PITCH;
-  static constexpr int STAGING = FUSED ? 4 * 2 * STAGE_BUF : 0;
-  static constexpr int BUDGET = (FUSED ? kSmemBudgetFused : kSmemBudget) - STAGING;
+  // fused-combine epilogue: each epilogue warp stages its 32 output rows (bf16,
+  // row pitch padded by 16 bytes so the lane-per-row writes are conflict-free);
+  // each row then leaves as one bulk async copy (TMA engine) to its destination
+  static constexpr int STAGE_PITCH = BN * 2 + 16;
+  static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 0;
+  static constexpr int BUDGET = kSmemBudget - STAGING;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
@@ -251,6 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int seq = 0;
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
+      int ready_seg = -1;            // (per-segment flags: the segment `ready` refers to)
       // (tile_ahead) the next tile id may be fetched one tile ahead, so the global
       // atomic's latency overlaps this tile's loads; off by default (measured slower)
       int next_tile = (leader && tile_ahead) ? (int)atomicAdd(sched, 1u) : 0;
@@ -287,6 +285,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // those generic-proxy arrivals before the TMA (async proxy) reads
           const int32_t* ss = sw.seg_src + (long long)seg * sw.G * 3;
           bool waited = false;
+          if (sw.per_seg && seg != ready_seg) {
+            ready = 0;
+            ready_seg = seg;
+          }
+          const unsigned* fl = sw.per_seg ? sw.flags + seg : sw.flags;
+          const int fstride = sw.per_seg ? 256 : 1;  // SigBlock::flag_seg[s][pos] / flag_data[s]
           for (int s = 0; s < sw.G; ++s) {
             if (s == sw.me || ((ready >> s) & 1ull)) continue;
             const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const unsigned long long t0 = globaltimer_ns();
             unsigned v;
             do {
-              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sw.flags + s) : "memory");
+              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl + s * fstride) : "memory");
               if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
                 atomicOr(err, kErrTimeout);
                 break;
@@ -422,7 +426,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // NVLink.  The warp stages its 32 rows in shared memory (16-byte granules,
         // XOR-swizzled by row), releases the accumulator, then writes row by row with
         // all 32 lanes so every NVLink store is a whole contiguous row segment.
-        uint8_t* stg = staging + (size_t)(warp - 2) * 2 * C::STAGE_BUF + (size_t)lane * C::STAGE_PITCH;
+        constexpr int PITCH = C::STAGE_PITCH;
+        uint8_t* stg = staging + (size_t)(warp - 2) * 32 * PITCH;
+        uint8_t* my_row = stg + (size_t)lane * PITCH;
         unsigned long long dst_row = 0;
         const int32_t* ss = fr.seg_src + (long long)seg * fr.G * 3;
         for (int s = 0; s < fr.G; ++s) {
@@ -433,31 +439,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             break;
           }
         }
+        bulk_wait_read_all();  // this lane's previous row copy has left the staging row
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t v[32];
           tmem_ld32(taddr + c, v);
-          uint8_t* buf = stg + ((c / 32) & 1) * C::STAGE_BUF;
-          // the copy that last read this buffer (two chunks ago) must have left it;
-          // at most the previous chunk's copy stays in flight
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            reinterpret_cast<uint4*>(buf)[i] =
+            reinterpret_cast<uint4*>(my_row)[c / 8 + i] =
                 make_uint4(pack_bf16x2(__uint_as_float(v[8 * i + 0]), __uint_as_float(v[8 * i + 1])),
                            pack_bf16x2(__uint_as_float(v[8 * i + 2]), __uint_as_float(v[8 * i + 3])),
                            pack_bf16x2(__uint_as_float(v[8 * i + 4]), __uint_as_float(v[8 * i + 5])),
                            pack_bf16x2(__uint_as_float(v[8 * i + 6]), __uint_as_float(v[8 * i + 7])));
-          fence_proxy_async_smem();
-          if (dst_row != 0) bulk_s2g(reinterpret_cast<void*>(dst_row + 2ull * c), smem_u32(buf), 64);
-          bulk_commit();  // (possibly empty) group per chunk keeps the wait arithmetic uniform
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {  // accumulator drained: the MMA may reuse it
+        if (lane == 0) {  // accumulator drained into smem: the MMA may reuse it
           if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
           else mbar_arrive(&tempty[acc]);
+        }
+        // every lane ships its own row (a contiguous BN-column segment of the
+        // destination row) with one bulk copy; the copy engine keeps the NVLink
+        // stores in flight while the warp moves on to the next accumulator
+        fence_proxy_async_smem();
+        if (dst_row != 0) {
+          bulk_s2g(reinterpret_cast<void*>(dst_row), smem_u32(my_row), BN * 2);
+          bulk_commit();
         }
       } else {
         uint16_t* drow = D + grow * ldd + (long long)nt * BN;

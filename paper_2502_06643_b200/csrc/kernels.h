@@ -17,6 +17,8 @@ struct SigBlock {
   unsigned flag_cnt[64];      // flag_cnt[s] = epoch once source s's count row landed
   unsigned flag_data[64];     // flag_data[s] = epoch once every row s sends here landed
   unsigned flag_y[64];        // flag_y[g] = epoch once rank g's expert outputs are ready
+  unsigned flag_seg[64][256]; // flag_seg[s][pos] = epoch once source s's rows of this rank's
+                              // pos-th hosted expert landed (slot-ordered push, k_push)
 };
 
 // Dispatch plan arguments shared by K2/K3/K8 (dispatch.cu).
@@ -65,16 +67,25 @@ struct PlanBuffers {
   // tp > 1: the tp partial outputs of one item live part_stride uint4 apart (virtual
   // mode: the expert-output buffers of the slices; fused combine: the return buffers)
   long long part_stride;
+  // slot-ordered P2P push (k_push): inverse of cslot_of_item, per-expert pushed-row
+  // counters, and the work table built by k_layout:
+  //   push_work[0] = items, push_work[1] = chunks, then per item (e, first chunk, pos of e
+  //   among its EP group's experts); items ordered (pos, destination group rotated by rank)
+  int32_t* item_of_slot;
+  int32_t* done_rows;
+  int32_t* push_work;
 };
 
 // K5 per-tile arrival waits (P2P overlap): the producer waits only for the source
 // ranks whose rows a tile reads; tiles holding only this rank's own rows run first.
 struct SrcWait {
-  const unsigned* flags;          // flag_data[G] of this rank; nullptr = no waits (all rows local)
+  const unsigned* flags;          // per_seg ? SigBlock::flag_seg [G][256] : flag_data [G] of this
+                                  // rank; nullptr = no waits (all rows local)
   const int32_t* seg_src;         // see PlanBuffers::seg_src
   int G;
   int me;
   unsigned epoch;
+  int per_seg;                    // 1: wait per (source, hosted segment) (slot-ordered push)
 };
 
 // K6 epilogue redirection (fused combine, P2P mode); enabled == 0 -> plain stores.
@@ -89,9 +100,13 @@ int plan_tiles(int T, int V);
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
 void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s);
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s);
-// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers
+// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers,
+// 3 = plan arrays only (+ item_of_slot), 4 = rows hosted here only (plan already built)
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
                     cudaStream_t s);
+// P2P: rows for peers in send order, chunk by chunk, raising flag_seg per (source, expert)
+// as each expert's rows complete (K5 consumes experts as they arrive).
+void launch_push(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int num_sms, cudaStream_t s);
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s);
 // P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);

@@ -98,7 +98,11 @@ struct moe_ctx {
   // P2P overlap: rows for peers are pushed on a side stream while K5 starts on
   // this rank's own rows (fork after the layout kernel, join in combine)
   cudaStream_t side = nullptr;
-  bool local_first = false;             // MOE_SCATTER_LOCAL_FIRST: own rows launched before the fork
+  // slot-ordered push (default; MOE_P2P_PUSH=tile selects the token-tile scatter)
+  bool push_slot = true;
+  int32_t* item_of_slot = nullptr;      // [max_tokens * k]
+  int32_t* done_rows = nullptr;         // [E]
+  int32_t* push_work = nullptr;         // [2 + 3E]
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   // last dispatch
@@ -168,6 +172,9 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.cslot_of_item = c->cslot_of_item;
   b.ret_local = reinterpret_cast<const uint4*>(c->retbuf);
   b.part_stride = c->virt ? c->cap_rows * c->H / 8 : c->send_rows * c->H / 8;
+  b.item_of_slot = c->item_of_slot;
+  b.done_rows = c->done_rows;
+  b.push_work = c->push_work;
   return b;
 }
 
@@ -392,11 +399,15 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->seg_src, sizeof(int32_t) * 3 * (size_t)E * G) &&
             A((void**)&ctx->cslot_base, sizeof(int32_t) * (size_t)E) &&
             A((void**)&ctx->cslot_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
-            A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G);
+            A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G) &&
+            A((void**)&ctx->item_of_slot, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
+            A((void**)&ctx->done_rows, sizeof(int32_t) * (size_t)E) &&
+            A((void**)&ctx->push_work, sizeof(int32_t) * (size_t)(2 + 3 * E));
   if (!ok) return bail(MOE_ERR_CUDA);
   cudaMemset(ctx->sig, 0, sizeof(SigBlock));
   cudaMemset(ctx->done_counter, 0, 4 * sizeof(unsigned));  // [0] scatter last-CTA, [2..3] GEMM scheduler
   cudaMemset(ctx->err_dev, 0, sizeof(int));
+  cudaMemset(ctx->done_rows, 0, sizeof(int32_t) * E);
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess) {
@@ -441,12 +452,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     sig[0] = ctx->sig;
     if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
       ctx->p2p = true;
-      int prio_lo = 0, prio_hi = 0;
-      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-      const char* sp = getenv("MOE_SIDE_PRIORITY");  // "high": the peers' rows get SMs first
-      const int prio = (sp && !strcmp(sp, "high")) ? prio_hi : prio_lo;
-      ctx->local_first = getenv("MOE_SCATTER_LOCAL_FIRST") && atoi(getenv("MOE_SCATTER_LOCAL_FIRST")) != 0;
-      if (cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, prio) != cudaSuccess ||
+      const char* pm = getenv("MOE_P2P_PUSH");
+      ctx->push_slot = !(pm && !strcmp(pm, "tile"));
+      if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         fail(ctx, MOE_ERR_CUDA, "side stream / event creation failed");
@@ -494,6 +502,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
         // fused combine of TP slice tpi lands in partial region tpi of the source's buffer
         ret[g] = static_cast<uint16_t*>(p[3]) + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
       }
+      // TEMPORARY timing experiment (wrong results): K6 fused stores stay local
+      if (getenv("MOE_DEBUG_FUSED_LOCAL"))
+        for (int g = 0; g < G; ++g) ret[g] = ctx->retbuf;
     }
     if (cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(ctx->src_table, src.data(), sizeof(void*) * src.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -526,7 +537,8 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
                  ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
-                 ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table};
+                 ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
+                 ctx->item_of_slot, ctx->done_rows, ctx->push_work};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -667,20 +679,29 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   if (ctx->p2p) {
     // rows for peers: NVLink stores on the side stream (arrival flags raised by its
     // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
-    if (ctx->local_first) {
+    if (ctx->push_slot) {
+      // plan arrays (+ the send-order inverse) first; then the peers' rows leave in
+      // send order on the side stream, expert by expert with per-expert arrival
+      // flags, while this rank's own rows are copied on `stream` and K5 starts
+      launch_scatter(a, x, idx, b, 3, s);
+      CU(cudaEventRecord(ctx->ev_fork, s));
+      CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      launch_push(a, x, b, ctx->num_sms, ctx->side);
+      tl_rec(ctx, 3, ctx->side);
+      CU(cudaEventRecord(ctx->ev_join, ctx->side));
+      launch_scatter(a, x, idx, b, 4, s);
+      tl_rec(ctx, 2, s);
+      LAUNCHED(ctx, 4);
+    } else {
+      CU(cudaEventRecord(ctx->ev_fork, s));
+      CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      launch_scatter(a, x, idx, b, 2, ctx->side);
+      tl_rec(ctx, 3, ctx->side);
+      CU(cudaEventRecord(ctx->ev_join, ctx->side));
       launch_scatter(a, x, idx, b, 1, s);
       tl_rec(ctx, 2, s);
+      LAUNCHED(ctx, 3);
     }
-    CU(cudaEventRecord(ctx->ev_fork, s));
-    CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-    launch_scatter(a, x, idx, b, 2, ctx->side);
-    tl_rec(ctx, 3, ctx->side);
-    CU(cudaEventRecord(ctx->ev_join, ctx->side));
-    if (!ctx->local_first) {
-      launch_scatter(a, x, idx, b, 1, s);
-      tl_rec(ctx, 2, s);
-    }
-    LAUNCHED(ctx, 3);
   } else {
     launch_scatter(a, x, idx, b, 0, s);
     tl_rec(ctx, 2, s);
@@ -794,8 +815,9 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (rec) CU(cudaEventRecord(ev[0], s));
   // P2P: K5's producer waits per tile for the source ranks whose rows the tile reads;
   // the tiles of this rank's own rows go first (overlapping the peers' NVLink pushes)
-  const SrcWait wait1{ctx->p2p ? ctx->sig->flag_data : nullptr, ctx->seg_src, ctx->G, ctx->me, ctx->epoch};
-  const SrcWait nowait{nullptr, nullptr, 0, 0, 0};
+  const SrcWait wait1{ctx->p2p ? (ctx->push_slot ? &ctx->sig->flag_seg[0][0] : ctx->sig->flag_data) : nullptr,
+                      ctx->seg_src, ctx->G, ctx->me, ctx->epoch, ctx->push_slot ? 1 : 0};
+  const SrcWait nowait{nullptr, nullptr, 0, 0, 0, 0};
   const FusedRet plain{nullptr, nullptr, 0, 0};
   // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
   // source rank's return buffer at the item's send-order slot -- the combine
@@ -1087,6 +1109,10 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
 moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out) {
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   CU(cudaSetDevice(ctx->cfg.device));
+  if (ctx->p2p) {  // the peers' rows of the last dispatch have landed here
+    CU(cudaStreamWaitEvent(ctx->last_stream, ctx->ev_join, 0));
+    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, ctx->err_dev, ctx->last_stream);
+  }
   CU(cudaStreamSynchronize(ctx->last_stream));
   const int E = ctx->E, H = ctx->H;
   std::vector<int32_t> meta(1 + 3 * E + 4);
