@@ -98,8 +98,11 @@ struct moe_ctx {
   // P2P overlap: rows for peers are pushed on a side stream while K5 starts on
   // this rank's own rows (fork after the layout kernel, join in combine)
   cudaStream_t side = nullptr;
-  // slot-ordered push (default; MOE_P2P_PUSH=tile selects the token-tile scatter)
-  bool push_slot = true;
+  // MOE_P2P_PUSH=slot: send-order push with per-(source, expert) arrival flags (k_push).
+  // Measured slower than the token-tile scatter at E64 4EP (6.87 vs 6.64 ms: the
+  // per-chunk system fences drain the NVLink pipeline and the push CTAs slow K5),
+  // so the default is the token-tile scatter with whole-source flags.
+  bool push_slot = false;
   int32_t* item_of_slot = nullptr;      // [max_tokens * k]
   int32_t* done_rows = nullptr;         // [E]
   int32_t* push_work = nullptr;         // [2 + 3E]
@@ -453,7 +456,7 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
       ctx->p2p = true;
       const char* pm = getenv("MOE_P2P_PUSH");
-      ctx->push_slot = !(pm && !strcmp(pm, "tile"));
+      ctx->push_slot = pm && !strcmp(pm, "slot");
       if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -502,9 +505,6 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
         // fused combine of TP slice tpi lands in partial region tpi of the source's buffer
         ret[g] = static_cast<uint16_t*>(p[3]) + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
       }
-      // TEMPORARY timing experiment (wrong results): K6 fused stores stay local
-      if (getenv("MOE_DEBUG_FUSED_LOCAL"))
-        for (int g = 0; g < G; ++g) ret[g] = ctx->retbuf;
     }
     if (cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(ctx->src_table, src.data(), sizeof(void*) * src.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
