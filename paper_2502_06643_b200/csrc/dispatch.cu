@@ -397,16 +397,18 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
   __shared__ uint4* dst_s[kMaxWorld];
   __shared__ unsigned last;
   // col_split CTAs share a token tile; each recomputes the (cheap) in-tile
-  // ranks and copies one slice of the hidden dimension
+  // ranks and copies one slice of the hidden dimension.  The grid may be smaller
+  // than tiles x col_split (persistent: each CTA loops over work units).
   const int split = mode == 3 ? 1 : a.col_split;  // mode 3 copies nothing: one CTA per tile
-  const int part = blockIdx.x % split;
-  const int tile = blockIdx.x / split;
-  int s, t0, t1, tile0;
-  tile_info(a, tile, s, t0, t1, tile0);
   const int nslots = a.p2p ? a.G : 2;
   for (int q = threadIdx.x; q < nslots; q += blockDim.x) dst_s[q] = b.dst_table[q];
+  for (int unit = blockIdx.x; unit < a.n_tiles * split; unit += gridDim.x) {
+  const int part = unit % split;
+  const int tile = unit / split;
+  int s, t0, t1, tile0;
+  tile_info(a, tile, s, t0, t1, tile0);
   tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && (mode == 0 || mode == 1 || mode == 3));
-  if (mode == 3) return;
+  if (mode == 3) continue;
   // P2P, tp > 1: slot p (an EP group) fans out to ranks p*tp .. p*tp+tp-1 (the TP
   // all-gather inside the dispatch); otherwise a slot is one destination buffer
   const bool fan = a.p2p && a.tp > 1;
@@ -459,6 +461,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const u
         }
       }
     }
+  }
+  __syncthreads();  // it / run are reused by the next work unit
   }
   if (a.p2p && (mode == 0 || mode == 2)) {
     // the last CTA to finish raises flag_data[me] on every rank
@@ -727,11 +731,12 @@ void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cu
   k_layout<<<1, kMaxExperts, 0, s>>>(a, b, (long long)cap_rows);
 }
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
-                    cudaStream_t s) {
+                    cudaStream_t s, int max_ctas) {
   const size_t smem = sizeof(int) * (kScatterThreads / 32) * a.E;
+  int grid = a.n_tiles * (mode == 3 ? 1 : a.col_split);
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (a.n_tiles > 0)
-    k_scatter<<<a.n_tiles * (mode == 3 ? 1 : a.col_split), kScatterThreads, smem, s>>>(a, (const uint4*)x, idx,
-                                                                                       b, mode);
+    k_scatter<<<grid, kScatterThreads, smem, s>>>(a, (const uint4*)x, idx, b, mode);
   else if (a.p2p && (mode == 0 || mode == 2))
     k_signal<<<1, 32, 0, s>>>(a, b, 1);
 }

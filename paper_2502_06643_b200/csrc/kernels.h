@@ -103,7 +103,7 @@ void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cu
 // mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers,
 // 3 = plan arrays only (+ item_of_slot), 4 = rows hosted here only (plan already built)
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
-                    cudaStream_t s);
+                    cudaStream_t s, int max_ctas = 0);  // max_ctas > 0: persistent grid of that size
 // P2P: rows for peers in send order, chunk by chunk, raising flag_seg per (source, expert)
 // as each expert's rows complete (K5 consumes experts as they arrive).
 void launch_push(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int num_sms, cudaStream_t s);

@@ -103,6 +103,9 @@ struct moe_ctx {
   // per-chunk system fences drain the NVLink pipeline and the push CTAs slow K5),
   // so the default is the token-tile scatter with whole-source flags.
   bool push_slot = false;
+  // CTAs of the peers'-rows scatter that overlaps K5 (0: one per tile x column
+  // slice).  Fewer CTAs leave more of each SM to K5; MOE_SCATTER_CTAS overrides.
+  int remote_ctas = 0;
   int32_t* item_of_slot = nullptr;      // [max_tokens * k]
   int32_t* done_rows = nullptr;         // [E]
   int32_t* push_work = nullptr;         // [2 + 3E]
@@ -457,6 +460,7 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       ctx->p2p = true;
       const char* pm = getenv("MOE_P2P_PUSH");
       ctx->push_slot = pm && !strcmp(pm, "slot");
+      if (const char* rc = getenv("MOE_SCATTER_CTAS")) ctx->remote_ctas = atoi(rc);
       if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -695,7 +699,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     } else {
       CU(cudaEventRecord(ctx->ev_fork, s));
       CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-      launch_scatter(a, x, idx, b, 2, ctx->side);
+      launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
       tl_rec(ctx, 3, ctx->side);
       CU(cudaEventRecord(ctx->ev_join, ctx->side));
       launch_scatter(a, x, idx, b, 1, s);
