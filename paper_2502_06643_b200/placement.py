@@ -168,3 +168,83 @@ def balanced(load, G):
     else:
         assign, _ = ilp1_heuristic(load, G)
     return assign.astype(np.int32)
+
+
+# ---------------------------------------------------------------------------
+# ILP 2 (Eqs. 8-15): place each layer's ILP-1 clusters on GPUs.
+# Host tooling for the placement-feedback loop: the routing
+# statistics come from the GPU (moe_route_stats + moe_stats_allreduce).
+
+def comm_costs(coact, assign, G):
+    """Eq. (9): C[l][c1][c2] = sum of R[l][e1][e2] over e1 in cluster c1 of layer l
+    and e2 in cluster c2 of layer l+1.  coact: int [L-1][E][E]; assign: int [L][E]."""
+    coact = np.asarray(coact, dtype=np.int64)
+    assign = np.asarray(assign)
+    L1 = coact.shape[0]
+    C = np.zeros((L1, G, G), dtype=np.int64)
+    for l in range(L1):
+        A = np.eye(G, dtype=np.int64)[assign[l]]        # [E][G] one-hot x_{c,e,l}
+        B = np.eye(G, dtype=np.int64)[assign[l + 1]]
+        C[l] = A.T @ coact[l] @ B
+    return C
+
+
+def _pair_max(Cl, p1, p2, G):
+    """max over ordered GPU pairs g1 != g2 of the volume C[c1][c2] moved from GPU
+    p1[c1] to GPU p2[c2] (uniform NVSwitch bandwidth: B constant)."""
+    V = np.zeros((G, G), dtype=np.int64)
+    np.add.at(V, (np.asarray(p1)[:, None].repeat(G, 1), np.asarray(p2)[None, :].repeat(G, 0)), Cl)
+    np.fill_diagonal(V, 0)                              # same-GPU traffic costs nothing
+    return int(V.max()) if G > 1 else 0
+
+
+def objective_o2(C, gpu_of_cluster):
+    """Eq. (8) read as in SPEC place_opt: sum over layer transitions of the max
+    over ordered GPU pairs g1 != g2 of the volume on that pair."""
+    C = np.asarray(C)
+    G = C.shape[1] if C.ndim == 3 else len(gpu_of_cluster[0])
+    return sum(_pair_max(C[l], gpu_of_cluster[l], gpu_of_cluster[l + 1], G) for l in range(C.shape[0]))
+
+
+def ilp2_dp(C, G, L):
+    """Exact minimiser of O2 over per-layer cluster->GPU bijections (Eqs. 14-15)
+    by dynamic programming over (layer, permutation) -- the chain structure of
+    Eq. (8) makes the relaxation without Eq. (13) exact.  Eq. (13) (equal expert
+    counts per GPU over all layers) is not enforced here; `balance_slack`
+    reports how far the result is from it.  Ties: lexicographically smallest
+    permutation sequence.  Intended for G <= 5 (G! states per layer)."""
+    import itertools
+    perms = list(itertools.permutations(range(G)))
+    P = len(perms)
+    if L == 1:
+        return np.array([perms[0]], dtype=np.int32)
+    # cost[l][i][j] = transition l with layer-l permutation i, layer-(l+1) permutation j
+    best = np.zeros(P, dtype=np.int64)
+    back = []
+    for l in range(L - 1):
+        trans = np.array([[_pair_max(C[l], perms[i], perms[j], G) for j in range(P)] for i in range(P)])
+        tot = best[:, None] + trans                      # [i][j]
+        arg = np.argmin(tot, axis=0)                     # first (smallest i) among ties
+        best = tot[arg, np.arange(P)]
+        back.append(arg)
+    j = int(np.argmin(best))
+    seq = [j]
+    for l in range(L - 2, -1, -1):
+        j = int(back[l][j])
+        seq.append(j)
+    seq.reverse()
+    return np.array([perms[i] for i in seq], dtype=np.int32)
+
+
+def expert_to_gpu(assign, gpu_of_cluster):
+    """Composite map expert_to_gpu[l][e] = gpu_of_cluster[l][assign[l][e]]."""
+    assign = np.asarray(assign)
+    gpu_of_cluster = np.asarray(gpu_of_cluster)
+    return np.stack([gpu_of_cluster[l][assign[l]] for l in range(assign.shape[0])]).astype(np.int32)
+
+
+def balance_slack(e2g, G):
+    """max_g |#{(l, e): e2g[l][e] == g} - E L / G| (Eq. 13 at slack 0)."""
+    e2g = np.asarray(e2g)
+    counts = np.bincount(e2g.ravel(), minlength=G)
+    return float(np.abs(counts - e2g.size / G).max())

@@ -72,3 +72,54 @@ def test_skewed_load_isolates_hot_expert():
     a = placement.balanced(load, 4)
     assert a.tolist() == [0, 1, 2, 2, 3, 2, 3, 3]
     assert sum(1 for v in a if v == a[0]) == 1
+
+
+# ---------------------------------------------------------------- ILP 2 (host tooling, NEXT-4)
+def test_comm_costs_spec_examples_and_conservation():
+    rng = np.random.default_rng(3)
+    L, E, G = 4, 8, 4
+    coact = rng.integers(0, 30, (L - 1, E, E))
+    assign = np.stack([rng.permutation(np.arange(E) % G) for _ in range(L)])
+    C = placement.comm_costs(coact, assign, G)
+    assert C.shape == (L - 1, G, G)
+    for l in range(L - 1):                                     # S: sum C[l] == sum transitions[l]
+        assert C[l].sum() == coact[l].sum()
+        ref = np.zeros((G, G), np.int64)                         # naive quadruple loop
+        for e1 in range(E):
+            for e2 in range(E):
+                ref[assign[l][e1], assign[l + 1][e2]] += coact[l][e1][e2]
+        assert np.array_equal(C[l], ref)
+    one = placement.comm_costs(coact, np.zeros((L, E), int), 1)  # G = 1: all mass in C[l][0][0]
+    assert np.array_equal(one[:, 0, 0], coact.sum(axis=(1, 2)))
+    two = placement.comm_costs(np.array([[[10, 0], [0, 10]]]), np.array([[0, 1], [0, 1]]), 2)
+    assert two.tolist() == [[[10, 0], [0, 10]]]
+
+
+def test_objective_o2_spec_examples():
+    C = np.array([[[10, 0], [0, 10]]])
+    assert placement.objective_o2(C, [[0, 1], [0, 1]]) == 0      # heavy pairs co-located
+    assert placement.objective_o2(C, [[0, 1], [1, 0]]) == 10     # crossing permutation
+    assert placement.objective_o2(np.zeros((0, 2, 2)), [[0, 1]]) == 0   # L = 1: empty sum
+
+
+def test_ilp2_dp_matches_exhaustive():
+    import itertools
+    rng = np.random.default_rng(4)
+    for G, L in [(2, 3), (3, 3), (3, 4), (4, 3)]:
+        perms = list(itertools.permutations(range(G)))
+        for _ in range(6):
+            C = rng.integers(0, 40, (L - 1, G, G))
+            best = min(placement.objective_o2(C, [perms[i] for i in seq])
+                       for seq in itertools.product(range(len(perms)), repeat=L))
+            got = placement.ilp2_dp(C, G, L)
+            assert all(sorted(p) == list(range(G)) for p in got)   # Eqs. 14-15
+            assert placement.objective_o2(C, got) == best
+
+
+def test_expert_to_gpu_and_balance():
+    assign = np.array([[0, 0, 1, 1], [1, 0, 0, 1]])
+    goc = np.array([[1, 0], [0, 1]])
+    e2g = placement.expert_to_gpu(assign, goc)
+    assert e2g.tolist() == [[1, 1, 0, 0], [1, 0, 0, 1]]
+    assert placement.balance_slack(e2g, 2) == 0.0
+    assert placement.balance_slack(np.array([[0, 0, 0, 1]]), 2) == 1.0
