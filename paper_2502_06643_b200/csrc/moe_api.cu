@@ -103,9 +103,12 @@ struct moe_ctx {
   // per-chunk system fences drain the NVLink pipeline and the push CTAs slow K5),
   // so the default is the token-tile scatter with whole-source flags.
   bool push_slot = false;
-  // CTAs of the peers'-rows scatter that overlaps K5 (0: one per tile x column
-  // slice).  Fewer CTAs leave more of each SM to K5; MOE_SCATTER_CTAS overrides.
-  int remote_ctas = 0;
+  // CTAs of the peers'-rows scatter that overlaps K5 (persistent grid; 0 = one per
+  // tile x column slice).  32 CTAs still fill NVLink and leave the other SMs to
+  // K5: D5 4EP step 6.24 ms vs 6.73 (one CTA per tile), 6.53 (16), 6.28 (64),
+  // 6.59 (128) in one run (profiles/r1_v13_timeline_ctas_*); Mixtral 4EP unchanged.
+  // MOE_SCATTER_CTAS overrides.
+  int remote_ctas = 32;
   int32_t* item_of_slot = nullptr;      // [max_tokens * k]
   int32_t* done_rows = nullptr;         // [E]
   int32_t* push_work = nullptr;         // [2 + 3E]
