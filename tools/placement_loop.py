@@ -127,41 +127,45 @@ def main():
 
     x0 = synth.hidden_states(T, H, a.seed, device=dev)[t0:t1].contiguous()
     bufs = [torch.empty_like(x0), torch.empty_like(x0)]
-    results = {}
-    for name, plan in plans.items():
-        wl = [weights_for([e for e in range(E) if plan[li][e] == rank]) for li in range(L)]
+    wls = {name: [weights_for([e for e in range(E) if plan[li][e] == rank]) for li in range(L)]
+           for name, plan in plans.items()}
 
-        def chain():
-            xin = x0
-            for li in range(L):
-                lay.route(logits[li], k, idx[li], w[li])
-                lay.dispatch(xin, idx[li], plan[li])
-                lay.expert_ffn(*wl[li])
-                out = bufs[li % 2]
-                lay.combine(w[li], out)
-                xin = out
+    def chain(plan, wl):
+        xin = x0
+        for li in range(L):
+            lay.route(logits[li], k, idx[li], w[li])
+            lay.dispatch(xin, idx[li], plan[li])
+            lay.expert_ffn(*wl[li])
+            out = bufs[li % 2]
+            lay.combine(w[li], out)
+            xin = out
 
-        chain()
-        torch.cuda.synchronize()
-        if N > 1:
-            dist.barrier()
-        times = []
-        for _ in range(a.reps):
+    for name, plan in plans.items():      # warm-up (also builds every weight set)
+        chain(plan, wls[name])
+    torch.cuda.synchronize()
+    # placements interleaved rep by rep, so clock drift under the power cap
+    # affects them alike; median over reps of the max over ranks
+    times = {name: [] for name in plans}
+    for _ in range(a.reps):
+        for name, plan in plans.items():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if N > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             e0.record()
-            chain()
+            chain(plan, wls[name])
             e1.record()
             torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        t = torch.tensor(times, dtype=torch.float64, device=dev)
+            times[name].append(e0.elapsed_time(e1))
+    results = {}
+    for name, plan in plans.items():
+        t = torch.tensor(times[name], dtype=torch.float64, device=dev)
         if N > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tm = float(t.mean())
+        tm = float(t.median())
         rows_max = [int(max(np.bincount(plan[li], weights=load_h[li], minlength=G))) for li in range(L)]
         results[name] = {"ms_per_chain": tm, "ms_per_layer": tm / L, "tokens_per_s": T * L / (tm * 1e-3),
+                         "reps_ms": [round(float(v), 3) for v in t.tolist()],
                          "o2_max_pair_tokens_summed": int(o2[name]),
                          "mean_max_gpu_rows": float(np.mean(rows_max)),
                          "balance_slack": placement.balance_slack(plan, G)}
