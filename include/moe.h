@@ -155,7 +155,13 @@ moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int
  * hosting its expert.  Collective when world > 1 (NCCL mode synchronises the
  * stream once to read the G x E count matrix).  The plan stays in the context
  * until the next moe_dispatch.  info: host, optional; if non-NULL the call
- * synchronises `stream` and fills it. */
+ * synchronises `stream` and fills it.
+ * CUDA graphs: a whole layer (moe_route .. moe_combine) may be captured and
+ * replayed on a stream (not in MOE_A2A_NCCL mode, whose dispatch reads the
+ * counts on the host).  In MOE_A2A_P2P mode the flag epoch lives on the device
+ * and advances once per dispatch, so every rank must replay its graph the same
+ * number of times, in the same order as its other collective calls; the
+ * placement must not change between capture and replay. */
 moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
                         const int32_t* expert_to_rank, moe_dispatch_info* info,
                         moe_stream_t stream);

@@ -65,6 +65,7 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 // Spin (system-scope acquire) until flags[0..n) >= epoch.  A peer that never
 // arrives (a rank that skipped a collective call, a dead process) latches
 // kErrTimeout after kFlagTimeoutNs instead of hanging the GPU.
+__device__ __forceinline__ unsigned cur_epoch(const unsigned* p) { return *(volatile const unsigned*)p; }
 __device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch, int* err) {
   for (int g = threadIdx.x; g < n; g += blockDim.x) {
     const uint64_t t0 = globaltimer_ns();
@@ -85,7 +86,8 @@ __device__ __forceinline__ unsigned* sig_flag(SigBlock* s, int which, int idx) {
 // via the caller's barrier, the CTA's prior writes visible system-wide)
 __device__ __forceinline__ void signal_all(const PlanArgs& a, const PlanBuffers& b, int which) {
   __threadfence_system();
-  for (int g = 0; g < a.G; ++g) st_release_sys(sig_flag(b.peer_sig[g], which, a.me), a.epoch);
+  const unsigned epoch = cur_epoch(a.epoch_ptr);
+  for (int g = 0; g < a.G; ++g) st_release_sys(sig_flag(b.peer_sig[g], which, a.me), epoch);
 }
 
 // ----------------------------------------------------------------- K2a: per-tile histogram
@@ -175,13 +177,21 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
   const int E = a.E;
   const int* cnt = b.cnt_all;
   if (a.p2p) {
+    // this dispatch's flag value: the device-side epoch advances here, once per
+    // dispatch, so a captured CUDA graph of the layer replays with fresh flags
+    if (threadIdx.x == 0) {
+      unsigned* ep = const_cast<unsigned*>(a.epoch_ptr);
+      *(volatile unsigned*)ep = cur_epoch(ep) + 1u;
+      __threadfence();
+    }
+    __syncthreads();
     if (e < E) {
       for (int g = 0; g < a.G; ++g) b.peer_sig[g]->cnt[a.me * E + e] = b.cnt_local[e];
       __threadfence_system();
     }
     __syncthreads();
     if (threadIdx.x == 0) signal_all(a, b, 0);
-    wait_flags_geq(b.my_sig->flag_cnt, a.G, a.epoch, b.err);
+    wait_flags_geq(b.my_sig->flag_cnt, a.G, cur_epoch(a.epoch_ptr), b.err);
     cnt = b.my_sig->cnt;
   }
   if (e < E) {
@@ -543,7 +553,8 @@ __global__ void __launch_bounds__(kScatterThreads) k_push(PlanArgs a, const uint
         b.done_rows[e] = 0;
         __threadfence_system();
         for (int q = 0; q < a.tp; ++q)
-          if (p * a.tp + q != a.me) st_release_sys(&b.peer_sig[p * a.tp + q]->flag_seg[a.me][info_s[3]], a.epoch);
+          if (p * a.tp + q != a.me)
+            st_release_sys(&b.peer_sig[p * a.tp + q]->flag_seg[a.me][info_s[3]], cur_epoch(a.epoch_ptr));
       }
     }
     __syncthreads();
@@ -596,7 +607,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const f
     w_s[i] = v < 0 ? 0.f : w[gi];
     slot_s[i] = a.fused ? 0 : b.slot_of_item[gi];
   }
-  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, a.epoch, b.err);
+  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, cur_epoch(a.epoch_ptr), b.err);
   __syncthreads();
   const int cpr = a.H / 8;
   const int cw = (cpr + a.col_split - 1) / a.col_split;
@@ -747,9 +758,11 @@ void launch_push(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
   k_signal<<<1, 32, 0, s>>>(a, b, which);
 }
-__global__ void k_wait(const unsigned* flags, int n, unsigned epoch, int* err) { wait_flags_geq(flags, n, epoch, err); }
-void launch_wait(const unsigned* flags, int n, unsigned epoch, int* err, cudaStream_t s) {
-  k_wait<<<1, 64, 0, s>>>(flags, n, epoch, err);
+__global__ void k_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err) {
+  wait_flags_geq(flags, n, cur_epoch(epoch_ptr), err);
+}
+void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, cudaStream_t s) {
+  k_wait<<<1, 64, 0, s>>>(flags, n, epoch_ptr, err);
 }
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s) {
   if (a.n_tiles <= 0) return;

@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int seq = 0;
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
       int ready_seg = -1;            // (per-segment flags: the segment `ready` refers to)
+      // P2P: this dispatch's flag value (written by k_layout earlier on the stream)
+      const unsigned epoch = sw.flags != nullptr ? *(volatile const unsigned*)sw.epoch_ptr : 0u;
       // (tile_ahead) the next tile id may be fetched one tile ahead, so the global
       // atomic's latency overlaps this tile's loads; off by default (measured slower)
       int next_tile = (leader && tile_ahead) ? (int)atomicAdd(sched, 1u) : 0;
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 atomicOr(err, kErrTimeout);
                 break;
               }
-            } while ((int)(v - sw.epoch) < 0);
+            } while ((int)(v - epoch) < 0);
             ready |= 1ull << s;
             waited = true;
           }

@@ -34,7 +34,8 @@ struct PlanArgs {
   int grp;      // this rank's EP group (me / tp)
   int virt;     // 1 = virtual ranks (every expert hosted by this process)
   int p2p;      // 1 = in-kernel NVLink peer stores/loads (real ranks)
-  unsigned epoch;  // P2P flag value of this dispatch
+  const unsigned* epoch_ptr;  // P2P: device word holding this dispatch's flag value
+                             // (k_layout increments it, so captured CUDA graphs replay correctly)
   int n_tiles;  // sum over sources of ceil(T_s / kTileTokens)
   int col_split;  // K3/K8: CTAs per token tile, each copying a slice of the hidden dim
   int seg_align;  // expert segments are padded to this many rows (= the GEMM M tile, 128 or 256)
@@ -84,7 +85,7 @@ struct SrcWait {
   const int32_t* seg_src;         // see PlanBuffers::seg_src
   int G;
   int me;
-  unsigned epoch;
+  const unsigned* epoch_ptr;      // see PlanArgs::epoch_ptr
   int per_seg;                    // 1: wait per (source, hosted segment) (slot-ordered push)
 };
 
@@ -111,7 +112,7 @@ void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uin
 // P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);
 // P2P: wait until flags[0..n) >= epoch (system-scope acquire).
-void launch_wait(const unsigned* flags, int n, unsigned epoch, int* err, cudaStream_t s);
+void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, cudaStream_t s);
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13,
                      cudaStream_t s);
 

@@ -81,7 +81,7 @@ struct moe_ctx {
   SigBlock* sig = nullptr;              // this rank's signal block (IPC-exported)
   unsigned* done_counter = nullptr;
   bool p2p = false;
-  unsigned epoch = 0;
+  unsigned* epoch_dev = nullptr;        // P2P flag value, advanced on the device by k_layout
   // GEMM M tile / segment padding: 256 rows (CTA pair) or, when the context's worst
   // case averages <= 256 routed rows per expert (decode-sized batches), 128 rows on
   // one CTA -- halving the MMA work spent on padding rows.  Fixed per context so
@@ -200,7 +200,7 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.grp = c->grp;
   a.virt = c->virt;
   a.p2p = c->p2p;
-  a.epoch = c->epoch;
+  a.epoch_ptr = c->epoch_dev;
   a.n_tiles = plan_tiles(T, c->V);
   a.seg_align = c->seg_align;
   a.fused = c->p2p && c->ffn_fused;
@@ -411,12 +411,14 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G) &&
             A((void**)&ctx->item_of_slot, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
             A((void**)&ctx->done_rows, sizeof(int32_t) * (size_t)E) &&
-            A((void**)&ctx->push_work, sizeof(int32_t) * (size_t)(2 + 3 * E));
+            A((void**)&ctx->push_work, sizeof(int32_t) * (size_t)(2 + 3 * E)) &&
+            A((void**)&ctx->epoch_dev, sizeof(unsigned));
   if (!ok) return bail(MOE_ERR_CUDA);
   cudaMemset(ctx->sig, 0, sizeof(SigBlock));
   cudaMemset(ctx->done_counter, 0, 4 * sizeof(unsigned));  // [0] scatter last-CTA, [2..3] GEMM scheduler
   cudaMemset(ctx->err_dev, 0, sizeof(int));
   cudaMemset(ctx->done_rows, 0, sizeof(int32_t) * E);
+  cudaMemset(ctx->epoch_dev, 0, sizeof(unsigned));
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess) {
@@ -545,7 +547,7 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
                  ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
                  ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
-                 ctx->item_of_slot, ctx->done_rows, ctx->push_work};
+                 ctx->item_of_slot, ctx->done_rows, ctx->push_work, ctx->epoch_dev};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -665,9 +667,13 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   if (ctx->tl_cur >= 0) ctx->tl_mask[ctx->tl_cur] = 0;
   tl_rec(ctx, 0, s);
   if (ctx->p2p) {
-    ++ctx->epoch;
-    // the previous layer's side-stream scatter reads plan arrays this call rewrites
-    CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    // the previous layer's side-stream scatter reads plan arrays this call rewrites.
+    // Inside a CUDA-graph capture the previous layer of the graph already joined the
+    // side stream in its moe_combine (and graph launches are serialised), and an
+    // event recorded outside the capture may not be waited on -- skip the wait.
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusNone) CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   }
   PlanArgs a = plan_args(ctx, T, k);
   PlanBuffers b = plan_buffers(ctx);
@@ -823,7 +829,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // P2P: K5's producer waits per tile for the source ranks whose rows the tile reads;
   // the tiles of this rank's own rows go first (overlapping the peers' NVLink pushes)
   const SrcWait wait1{ctx->p2p ? (ctx->push_slot ? &ctx->sig->flag_seg[0][0] : ctx->sig->flag_data) : nullptr,
-                      ctx->seg_src, ctx->G, ctx->me, ctx->epoch, ctx->push_slot ? 1 : 0};
+                      ctx->seg_src, ctx->G, ctx->me, ctx->epoch_dev, ctx->push_slot ? 1 : 0};
   const SrcWait nowait{nullptr, nullptr, 0, 0, 0, 0};
   const FusedRet plain{nullptr, nullptr, 0, 0};
   // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
@@ -929,7 +935,7 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
     // join the side-stream scatter first (never spin on a flag another kernel of
     // this GPU raises), then wait for the peers' rows
     CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, ctx->err_dev, s);
+    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch_dev, ctx->err_dev, s);
     LAUNCHED(ctx, 1);
   }
   const size_t ybytes = (size_t)ctx->cap_rows * ctx->H * 2;
@@ -1118,7 +1124,7 @@ moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, 
   CU(cudaSetDevice(ctx->cfg.device));
   if (ctx->p2p) {  // the peers' rows of the last dispatch have landed here
     CU(cudaStreamWaitEvent(ctx->last_stream, ctx->ev_join, 0));
-    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch, ctx->err_dev, ctx->last_stream);
+    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch_dev, ctx->err_dev, ctx->last_stream);
   }
   CU(cudaStreamSynchronize(ctx->last_stream));
   const int E = ctx->E, H = ctx->H;

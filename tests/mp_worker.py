@@ -107,6 +107,42 @@ def main():
     lay.sync()
     assert np.array_equal(load.cpu().numpy(), np.bincount(ridx.ravel(), minlength=E))
 
+    # CUDA-graph capture of a P2P layer: the flags carry a device-side epoch, so
+    # replays of the captured layer match the eager result bit-exactly
+    if lay.a2a == "p2p":
+        P = placements[1]
+        hosted = [e for e in range(E) if P[e] == rank]
+        w1, w3, w2 = inp.device_weights(dev, hosted) if hosted else (None, None, None)
+        w13 = moe.pack_w13(w1, w3) if hosted else None
+        idx = torch.empty(b - a, k, dtype=torch.int32, device=dev)
+        w = torch.empty(b - a, k, dtype=torch.float32, device=dev)
+        out = torch.empty(b - a, H, dtype=torch.bfloat16, device=dev)
+
+        def layer_step():
+            lay.route(logits, k, idx, w)
+            lay.dispatch(x, idx, P)
+            lay.expert_ffn(w13, w2)
+            lay.combine(w, out)
+
+        layer_step()
+        lay.sync()
+        ref = out.clone()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            layer_step()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            layer_step()
+        for _ in range(3):
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(out.view(torch.int16), ref.view(torch.int16)), "graph replay"
+        lay.sync()
+        del g
+
     # degenerate split: fewer tokens than ranks, so some ranks own 0 tokens (G7)
     # but still take part in every collective call; repeated layers reuse the
     # buffers (P2P epochs advance)
