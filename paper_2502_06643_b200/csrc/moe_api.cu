@@ -113,6 +113,10 @@ struct moe_ctx {
   int32_t* done_rows = nullptr;         // [E]
   int32_t* push_work = nullptr;         // [2 + 3E]
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the same pair for layers captured into a CUDA graph (an event recorded inside a
+  // capture must not be waited on by eager work afterwards); cur_join = the join
+  // event of the last dispatch
+  cudaEvent_t ev_fork_cap = nullptr, ev_join_cap = nullptr, cur_join = nullptr;
 
   // last dispatch
   bool have_plan = false;
@@ -468,7 +472,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       if (const char* rc = getenv("MOE_SCATTER_CTAS")) ctx->remote_ctas = atoi(rc);
       if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+          cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_fork_cap, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->ev_join_cap, cudaEventDisableTiming) != cudaSuccess) {
         fail(ctx, MOE_ERR_CUDA, "side stream / event creation failed");
         return bail(MOE_ERR_CUDA);
       }
@@ -543,6 +549,8 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_fork_cap) cudaEventDestroy(ctx->ev_fork_cap);
+  if (ctx->ev_join_cap) cudaEventDestroy(ctx->ev_join_cap);
   void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
                  ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
@@ -666,14 +674,22 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   ctx->tl_cur = ctx->tl_used < (int)ctx->tl_mask.size() ? ctx->tl_used : -1;
   if (ctx->tl_cur >= 0) ctx->tl_mask[ctx->tl_cur] = 0;
   tl_rec(ctx, 0, s);
+  cudaEvent_t ev_fork = ctx->ev_fork, ev_join = ctx->ev_join;
   if (ctx->p2p) {
     // the previous layer's side-stream scatter reads plan arrays this call rewrites.
     // Inside a CUDA-graph capture the previous layer of the graph already joined the
     // side stream in its moe_combine (and graph launches are serialised), and an
-    // event recorded outside the capture may not be waited on -- skip the wait.
+    // event recorded outside the capture may not be waited on -- skip the wait and
+    // fork/join through the capture-only events.
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CU(cudaStreamIsCapturing(s, &cs));
-    if (cs == cudaStreamCaptureStatusNone) CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    if (cs == cudaStreamCaptureStatusNone) {
+      CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    } else {
+      ev_fork = ctx->ev_fork_cap;
+      ev_join = ctx->ev_join_cap;
+    }
+    ctx->cur_join = ev_join;
   }
   PlanArgs a = plan_args(ctx, T, k);
   PlanBuffers b = plan_buffers(ctx);
@@ -697,20 +713,20 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
       // send order on the side stream, expert by expert with per-expert arrival
       // flags, while this rank's own rows are copied on `stream` and K5 starts
       launch_scatter(a, x, idx, b, 3, s);
-      CU(cudaEventRecord(ctx->ev_fork, s));
-      CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      CU(cudaEventRecord(ev_fork, s));
+      CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
       launch_push(a, x, b, ctx->num_sms, ctx->side);
       tl_rec(ctx, 3, ctx->side);
-      CU(cudaEventRecord(ctx->ev_join, ctx->side));
+      CU(cudaEventRecord(ev_join, ctx->side));
       launch_scatter(a, x, idx, b, 4, s);
       tl_rec(ctx, 2, s);
       LAUNCHED(ctx, 4);
     } else {
-      CU(cudaEventRecord(ctx->ev_fork, s));
-      CU(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+      CU(cudaEventRecord(ev_fork, s));
+      CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
       launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
       tl_rec(ctx, 3, ctx->side);
-      CU(cudaEventRecord(ctx->ev_join, ctx->side));
+      CU(cudaEventRecord(ev_join, ctx->side));
       launch_scatter(a, x, idx, b, 1, s);
       tl_rec(ctx, 2, s);
       LAUNCHED(ctx, 3);
@@ -934,7 +950,7 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   if (ctx->p2p) {
     // join the side-stream scatter first (never spin on a flag another kernel of
     // this GPU raises), then wait for the peers' rows
-    CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+    CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));
     launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch_dev, ctx->err_dev, s);
     LAUNCHED(ctx, 1);
   }
@@ -992,7 +1008,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
     ++ctx->tl_used;
     ctx->tl_cur = -1;
   }
-  if (ctx->p2p) CU(cudaStreamWaitEvent(s, ctx->ev_join, 0));  // join the side stream
+  if (ctx->p2p) CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));  // join the side stream
   return MOE_OK;
 }
 
@@ -1123,7 +1139,7 @@ moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, 
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   CU(cudaSetDevice(ctx->cfg.device));
   if (ctx->p2p) {  // the peers' rows of the last dispatch have landed here
-    CU(cudaStreamWaitEvent(ctx->last_stream, ctx->ev_join, 0));
+    CU(cudaStreamWaitEvent(ctx->last_stream, ctx->cur_join, 0));
     launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch_dev, ctx->err_dev, ctx->last_stream);
   }
   CU(cudaStreamSynchronize(ctx->last_stream));

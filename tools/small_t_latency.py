@@ -40,14 +40,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    uid = None
     if N > 1:
         dist.init_process_group("nccl", device_id=dev)
+
+    def fresh_uid():  # one NCCL unique id per context
+        if N == 1:
+            return None
         u = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             u.copy_(torch.frombuffer(bytearray(moe.get_unique_id()), dtype=torch.uint8))
         dist.broadcast(u, 0)
-        uid = bytes(u.cpu().numpy().tobytes())
+        return bytes(u.cpu().numpy().tobytes())
     H, F, E, k = a.H, a.F, a.E, a.k
     Ts = [int(t) for t in a.tokens.split(",")]
     Tmax = max(Ts)
@@ -63,7 +66,7 @@ def main():
         t0, t1 = rank * T // N, (rank + 1) * T // N
         Tr = t1 - t0
         lay = moe.MoeLayer(max_tokens=max(T // N + 1, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N,
-                           rank=rank, device=local, uid=uid, a2a="p2p" if N > 1 else "nccl")
+                           rank=rank, device=local, uid=fresh_uid(), a2a="p2p" if N > 1 else "nccl")
         x = synth.hidden_states(T, H, 1, device=dev)[t0:t1].contiguous()
         logits = synth.zipf_logits(T, E, 1.6, 1, device=dev)[t0:t1].contiguous()
         prev = synth.zipf_logits(T, E, 1.6, 2, device=dev)[t0:t1].contiguous()
