@@ -33,11 +33,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--a2a", default="p2p")
+    ap.add_argument("--tokens", type=int, default=0, help="override the config's total token count")
     a = ap.parse_args()
     from paper_2502_06643_b200 import moe, placement
 
     cfg = CONFIGS[a.config]
     E, k, H, F, T = cfg["E"], cfg["k"], cfg["H"], cfg["F"], cfg["T"]
+    T = a.tokens or T
     rank = int(os.environ.get("RANK", 0))
     N = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -97,7 +99,7 @@ def main():
         step()
     rec = np.array(lay.timeline_read())
     med = np.median(rec, axis=0)
-    print(json.dumps({"rank": rank, "config": a.config, "placement": a.placement, "tp": tp,
+    print(json.dumps({"rank": rank, "config": a.config, "tokens": T, "placement": a.placement, "tp": tp,
                       "env": {kk: v for kk, v in os.environ.items() if kk.startswith("MOE_")},
                       "median_ms": dict(zip(moe.MoeLayer.TIMELINE, [round(float(v), 4) for v in med]))}),
           flush=True)
