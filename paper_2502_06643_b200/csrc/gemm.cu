@@ -534,7 +534,7 @@ int gemm_block_n(int N, bool swiglu) {
   return 64;
 }
 
-int gemm_b_box_rows(int N, bool swiglu, int cg, int bn) { return (bn > 0 ? bn : gemm_block_n(N, swiglu)) / cg; }
+int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu) / cg; }
 
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
@@ -596,8 +596,8 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
-                                unsigned* sched, const FusedRet& fr, cudaStream_t s, int bn_override) {
-  const int bn = (bn_override > 0 && !swiglu) ? bn_override : gemm_block_n(N, swiglu);
+                                unsigned* sched, const FusedRet& fr, cudaStream_t s) {
+  const int bn = gemm_block_n(N, swiglu);
   const bool fused = fr.enabled && !swiglu;
 #define MOE_GO(BN_, SW_, CG_, FU_) \
   launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s)

@@ -118,9 +118,7 @@ void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H
 
 // K5/K6 grouped GEMM (gemm.cu).
 int gemm_block_n(int N, bool swiglu);
-// TMA box rows of the B (weight) operand per CTA; bn > 0 overrides the tile width
-// (plain GEMMs only: 64, 128 or 256, dividing N)
-int gemm_b_box_rows(int N, bool swiglu, int cg, int bn = 0);
+int gemm_b_box_rows(int N, bool swiglu, int cg);  // TMA box rows of the B (weight) operand per CTA
 int pack_block(int F);
 // Launch the persistent grouped GEMM: D[rows][ldd] for every hosted expert segment.
 // tmA / tmB are CUtensorMap (128 bytes each) built by make_tmap_2d.  If wait_flags is
@@ -129,7 +127,7 @@ int pack_block(int F);
 // small token counts); must match the segment padding of the dispatch layout.
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
-                                unsigned* sched, const FusedRet& fr, cudaStream_t s, int bn = 0);
+                                unsigned* sched, const FusedRet& fr, cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.

@@ -64,7 +64,6 @@ struct moe_ctx {
   const void* tmB1_ptr = nullptr;
   const void* tmB2_ptr = nullptr;
   int tmB_nw = -1;
-  int tmB_bn6 = -1;
 
   // optional K5/K6 timing event records (3 events per moe_expert_ffn call)
   std::vector<cudaEvent_t> ev;
@@ -826,23 +825,8 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const int H = ctx->H, F = ctx->Fl, tp = ctx->tp;
   const bool vslices = ctx->virt && tp > 1;  // virtual TP: K6 once per FFN slice
   const int nw_rows = ctx->virt ? ctx->E : nw;
-  // Decode-sized contexts (128-row tiles, about one M tile per expert): K6 has only
-  // n_w x H/BN tiles, each streaming a BN x F slab of W2 -- with BN = 256 and 2
-  // hosted experts that is 32 tiles, i.e. 32 SMs pulling the weights at their
-  // per-SM rate.  Narrow the tile until the grid covers the SMs.  (K5's width is
-  // tied to the W1/W3 packing and stays.)
-  int bn6 = 0;
-  if (ctx->gemm_cg == 1 && !vslices) {
-    bn6 = 64;
-    for (int cand : {256, 128})
-      if (H % cand == 0 && (long long)nw * (H / cand) >= ctx->num_sms) {
-        bn6 = cand;
-        break;
-      }
-    if (const char* e6 = getenv("MOE_DECODE_K6_BN")) bn6 = atoi(e6);
-  }
-  if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows || ctx->tmB_bn6 != bn6) {
-    const int bn1 = gemm_b_box_rows(2 * F, true, ctx->gemm_cg), bn2 = gemm_b_box_rows(H, false, ctx->gemm_cg, bn6);
+  if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows) {
+    const int bn1 = gemm_b_box_rows(2 * F, true, ctx->gemm_cg), bn2 = gemm_b_box_rows(H, false, ctx->gemm_cg);
     if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)nw_rows * 2 * F, H, bn1) ||
         !make_tmap_2d(ctx->tmB2, w2, (uint64_t)nw_rows * H, F, bn2))
       return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weights");
@@ -853,7 +837,6 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     ctx->tmB1_ptr = w13;
     ctx->tmB2_ptr = w2;
     ctx->tmB_nw = nw_rows;
-    ctx->tmB_bn6 = bn6;
   }
   tl_rec(ctx, 4, s);
   const bool rec = ctx->timing_used < (int)ctx->ev.size() / 3;
@@ -877,7 +860,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   tl_rec(ctx, 5, s);
   if (!vslices) {
     e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
-                            ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s, bn6);
+                            ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s);
     if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
   } else {
     // partial output of FFN slice q (h columns and W2 columns [q F/tp, (q+1) F/tp))
