@@ -190,6 +190,8 @@ def run_layer(lay, inp, P, G):
     (700, 128, 256, 16, 4, 4, [e % 4 for e in range(16)]),
     (600, 128, 128, 64, 8, 8, [e // 8 for e in range(64)]),   # D5 shape family (E64 top-8), 8 virtual ranks
     (333, 64, 64, 5, 5, 1, [0] * 5),                         # k = E, ragged everything, BN = 64 tiles
+    (97, 64, 128, 256, 16, 4, [(7 * e) % 4 for e in range(256)]),  # maximum E and k (kMaxExperts, kMaxK)
+    (1, 64, 128, 8, 2, 1, [0] * 8),                          # a single token
 ])
 def test_layer_parity(cuda_ok, T, H, F, E, k, G, P):
     inp = Inputs(T, H, F, E, k, s=1.6, seed=11)
