@@ -264,3 +264,66 @@ def test_mixtral_layer_full_size_sampled(cuda_ok):
     ref, ridx, rw = olayer.layer_direct(xs, ls, k, fn)
     assert np.array_equal(idx[sel].cpu().numpy(), ridx)
     assert_close_layer(bf16_to_f64(out[sel]), ref)
+
+
+def test_cuda_graph_replay_bit_exact(cuda_ok):
+    """A whole layer (route .. combine) captured in a CUDA graph replays to the
+    eager result bit-exactly (no host round trip on the path; moe.h)."""
+    moe = _moe()
+    T, H, F, E, k, G = 700, 128, 256, 8, 2, 4
+    P = [0, 1, 2, 2, 3, 2, 3, 3]
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=29)
+    lay = make_layer(T, H, F, E, k, G)
+    x, logits = inp.to_device(DEV)
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E)))
+    w13 = moe.pack_w13(w1, w3)
+    idx = torch.empty(T, k, dtype=torch.int32, device=DEV)
+    w = torch.empty(T, k, dtype=torch.float32, device=DEV)
+    out = torch.empty(T, H, dtype=torch.bfloat16, device=DEV)
+
+    def step():
+        lay.route(logits, k, idx, w)
+        lay.dispatch(x, idx, P)
+        lay.expert_ffn(w13, w2)
+        lay.combine(w, out)
+
+    step()
+    lay.sync()
+    ref = out.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int16), ref.view(torch.int16))
+    lay.sync()
+
+
+def test_timeline_events_ordered(cuda_ok):
+    """moe_timeline_*: 8 events per layer, non-decreasing along the stream order."""
+    moe = _moe()
+    T, H, F, E, k, G = 500, 128, 256, 8, 2, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=31)
+    lay = make_layer(T, H, F, E, k, G)
+    x, logits = inp.to_device(DEV)
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E)))
+    w13 = moe.pack_w13(w1, w3)
+    lay.timeline(3)
+    for _ in range(4):                 # one more layer than records: the extra is not recorded
+        idx, w = lay.route(logits, k)
+        lay.dispatch(x, idx, [0, 1] * 4)
+        lay.expert_ffn(w13, w2)
+        lay.combine(w)
+    rec = lay.timeline_read()
+    assert len(rec) == 3
+    for r in rec:
+        assert r[0] == 0.0 and all(v >= 0 for v in r)
+        main = [r[0], r[1], r[2], r[4], r[5], r[6], r[7]]   # events on the caller's stream
+        assert all(b >= a for a, b in zip(main, main[1:]))
