@@ -734,6 +734,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   } else {
     launch_scatter(a, x, idx, b, 0, s);
     tl_rec(ctx, 2, s);
+    tl_rec(ctx, 3, s);  // no separate peers' scatter: same as event 2
     LAUNCHED(ctx, 2);
   }
   if (nccl) {
