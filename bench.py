@@ -196,6 +196,18 @@ def oracle_time(cfg, n_tok, reps, seed, s, G, P, state=None, tp=1):
     return times, state
 
 
+def host_threads():
+    """BLAS thread-pool limit covering the host's cores.  torchrun exports
+    OMP_NUM_THREADS=1 to every rank, which would pin the oracle (the reference
+    arm / cpu_baseline) to one core; the oracle runs on the box's host cores."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=os.cpu_count())
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def threads_used():
     try:
         from threadpoolctl import threadpool_info
@@ -532,9 +544,11 @@ def run_ours(args):
                                    "then moe_stats_allreduce; synth.multilayer_logits (dependency 0.5)"},
         }
         if N == 1 and not args.no_cpu_baseline:
-            times, _ = oracle_time(cfg, args.cpu_tokens, args.cpu_reps, args.seed, s, 1, np.zeros(E, np.int32))
+            with host_threads():
+                times, _ = oracle_time(cfg, args.cpu_tokens, args.cpu_reps, args.seed, s, 1, np.zeros(E, np.int32))
+                cores = threads_used()
             line["cpu_baseline"] = {
-                "value": args.cpu_tokens * len(times) / sum(times), "unit": "tokens/s", "cores": threads_used(),
+                "value": args.cpu_tokens * len(times) / sum(times), "unit": "tokens/s", "cores": cores,
                 "kind": "oracle",
                 "sample": f"{args.cpu_reps} x {args.cpu_tokens} random tokens of the same workload through "
                           f"oracle.layer.layer_ep (float64 numpy, G=1); weights pre-converted bf16->float64 "
@@ -562,8 +576,11 @@ def run_reference(args):
     P = np.array([e // (E // G) for e in range(E)], dtype=np.int32)
     state = oracle_setup(cfg, args.seed, args.zipf_s, G, P)
     if args.warmup:
-        oracle_time(cfg, args.ref_tokens, min(args.warmup, 3), args.seed, args.zipf_s, G, P, state, tp)
-    times, _ = oracle_time(cfg, args.ref_tokens, args.steps, args.seed + 1, args.zipf_s, G, P, state, tp)
+        with host_threads():
+            oracle_time(cfg, args.ref_tokens, min(args.warmup, 3), args.seed, args.zipf_s, G, P, state, tp)
+    with host_threads():
+        times, _ = oracle_time(cfg, args.ref_tokens, args.steps, args.seed + 1, args.zipf_s, G, P, state, tp)
+        cores = threads_used()
     total = sum(times)
     val = args.ref_tokens * len(times) / total
     ms = total / len(times) * 1e3
@@ -573,7 +590,7 @@ def run_reference(args):
             "config": {"workload": cfg["workload"], "experts": E, "top_k": cfg["k"], "hidden": cfg["H"],
                        "ffn": cfg["F"], "tokens_total": cfg["T"], "ep": G, "tp": tp, "placement": "contiguous",
                        "zipf_s": args.zipf_s},
-            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": threads_used(), "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step = {args.ref_tokens} random tokens of the workload through "
                                        f"oracle.layer.layer_ep{'_tp' if tp > 1 else ''} (float64 numpy) on the host "
                                        f"cores"},
