@@ -398,7 +398,7 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
 // mode: 0 every row; (P2P overlap) 1 = rows this rank hosts, plus the plan
 // arrays; 2 = rows for peers only (runs on a side stream next to K5, whose
 // producer waits per tile for the sources it needs), last CTA raises flag_data.
-__global__ void __launch_bounds__(kScatterThreads) k_scatter(PlanArgs a, const uint4* __restrict__ x,
+__global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, const uint4* __restrict__ x,
                                                              const int32_t* __restrict__ idx, PlanBuffers b,
                                                              int mode) {
   __shared__ TileItems it;
@@ -581,7 +581,7 @@ __global__ void k_signal(PlanArgs a, PlanBuffers b, int which) {
 // thread; the accumulation order is still j ascending.  In P2P mode the rows
 // are read from the hosting rank's expert-output buffer over NVLink.
 template <int KT>
-__global__ void __launch_bounds__(kScatterThreads) k_combine(PlanArgs a, const float* __restrict__ w, PlanBuffers b,
+__global__ void __launch_bounds__(kScatterThreads, 2) k_combine(PlanArgs a, const float* __restrict__ w, PlanBuffers b,
                                                              uint4* __restrict__ out) {
   __shared__ int row_s[kMaxTileItems];
   __shared__ float w_s[kMaxTileItems];
