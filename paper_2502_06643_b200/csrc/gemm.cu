@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
                    int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf,
-                   int tile_ahead) {
+                   int tile_ahead, int ksplit, float* __restrict__ part, long long part_stride) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   extern __shared__ uint8_t smem_raw[];
@@ -218,7 +218,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total_tiles = sg.totalA + sg.tB0[sg.nseg];
+  // split-K (decode-sized contexts whose tiles cannot cover the SMs): tile id t =
+  // output tile t / ksplit, K slice t % ksplit; each slice's fp32 partial goes to
+  // part[slice] and k_splitk_reduce sums the slices in order (deterministic)
+  const int total_tiles = (sg.totalA + sg.tB0[sg.nseg]) * ksplit;
 
   // Dynamic tile scheduler: the leader's producer takes the next tile id from a
   // global counter (atomicAdd) and publishes it through an mbarrier ring to
@@ -278,7 +281,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         if (tile >= total_tiles) break;
         int arow, wrow, nt, seg;
-        decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt, seg);
+        decode_tile(sg, ntn, C::TILE_M, group_m, tile / ksplit, arow, wrow, nt, seg);
+        const int ks = tile % ksplit;
+        const int kb_lo = ks * nkb / ksplit, kb_hi = (ks + 1) * nkb / ksplit;
         const int a_row = arow + (int)crank * 128;
         const int b_row = wrow + nt * BN + (int)crank * C::B_ROWS;
         if (sw.flags != nullptr) {
@@ -313,12 +318,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         // L2 prefetch `pf` k-blocks ahead of the loads: the first cluster to touch a
         // weight tile would otherwise stall on DRAM latency for each of its k-blocks
-        for (int kb = 0; kb < min(pf, nkb); ++kb) {
+        for (int kb = kb_lo; kb < min(kb_lo + pf, kb_hi); ++kb) {
           tma_prefetch_l2_2d(&tmA, kb * BK, a_row);
           tma_prefetch_l2_2d(&tmB, kb * BK, b_row);
         }
-        for (int kb = 0; kb < nkb; ++kb) {
-          if (pf > 0 && kb + pf < nkb) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          if (pf > 0 && kb + pf < kb_hi) {
             tma_prefetch_l2_2d(&tmA, (kb + pf) * BK, a_row);
             tma_prefetch_l2_2d(&tmB, (kb + pf) * BK, b_row);
           }
@@ -356,7 +361,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        const int ks = tile % ksplit;
+        const int kb_lo = ks * nkb / ksplit, kb_hi = (ks + 1) * nkb / ksplit;
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smA + stage * C::A_BYTES);
@@ -364,8 +371,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = umma_desc_sw128(a_addr + kk * 32), bd = umma_desc_sw128(b_addr + kk * 32);
-            if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-            else umma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            const uint32_t accum = (kb != kb_lo || kk != 0) ? 1u : 0u;
+            if constexpr (CG == 2) umma_bf16_pair(d_tmem, ad, bd, idesc, accum);
+            else umma_bf16(d_tmem, ad, bd, idesc, accum);
           }
           if constexpr (CG == 2) umma_commit_pair_mc(&empty[stage], 0x3);
           else umma_commit(&empty[stage]);
@@ -395,12 +403,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (lane == 0) release_tile(seq);
       if (tile >= total_tiles) break;
       int arow, wrow, nt, seg;
-      decode_tile(sg, ntn, C::TILE_M, group_m, tile, arow, wrow, nt, seg);
+      decode_tile(sg, ntn, C::TILE_M, group_m, tile / ksplit, arow, wrow, nt, seg);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const long long grow = arow + (int)crank * 128 + q * 32 + lane;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      if constexpr (SWIGLU) {
+      if (ksplit > 1) {
+        // fp32 partial of K slice tile % ksplit (raw accumulators; the reduction
+        // kernel applies the epilogue)
+        float* prow = part + (long long)(tile % ksplit) * part_stride + grow * N + (long long)nt * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
+          tmem_ld_wait();
+          float4* dst = reinterpret_cast<float4*>(prow + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                 __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        }
+      } else if constexpr (SWIGLU) {
         uint16_t* drow = D + grow * ldd + (long long)nt * (BN / 2);
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
@@ -485,6 +508,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
         }
       }
+      if (FUSED && ksplit > 1) {  // (never launched: split-K is not combined with the fused combine)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
+          else mbar_arrive(&tempty[acc]);
+        }
+      }
       if constexpr (!FUSED) {
         tc_fence_before();
         __syncwarp();
@@ -539,7 +570,7 @@ int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu)
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const SrcWait& sw, int* err, unsigned* sched,
-                               const FusedRet& fr, cudaStream_t s) {
+                               const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride) {
   using C = GemmCfg<BN, CG, FUSED>;
   auto kern = k_grouped_gemm<BN, SWIGLU, CG, FUSED>;
   static bool configured = false;
@@ -591,16 +622,19 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
     ahead = (env && atoi(env) != 0) ? 1 : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
-                            sched, fr, pf, ahead);
+                            sched, fr, pf, ahead, ksplit, part, part_stride);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
-                                unsigned* sched, const FusedRet& fr, cudaStream_t s) {
+                                unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit, float* part,
+                                long long part_stride) {
   const int bn = gemm_block_n(N, swiglu);
+  if (ksplit < 1) ksplit = 1;
   const bool fused = fr.enabled && !swiglu;
 #define MOE_GO(BN_, SW_, CG_, FU_) \
-  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s)
+  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s, ksplit, part, \
+                                  part_stride)
 #define MOE_GO2(BN_, CG_) (fused ? MOE_GO(BN_, false, CG_, true) : MOE_GO(BN_, false, CG_, false))
   if (cg == 2) {
     if (swiglu) return bn == 256 ? MOE_GO(256, true, 2, false) : MOE_GO(128, true, 2, false);
@@ -614,6 +648,43 @@ cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, i
   return MOE_GO2(64, 1);
 #undef MOE_GO2
 #undef MOE_GO
+}
+
+// Split-K reduction (plain GEMM): D[row][c] = bf16( sum_{slice ascending} part[slice][row][c] )
+// over every row of every segment's padded M range (fp32, fixed order).
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ part, long long part_stride, int S,
+                                                       const int32_t* __restrict__ seg_meta, int E, int N, int tile_m,
+                                                       uint16_t* __restrict__ D, int ldd) {
+  const int nseg = seg_meta[0];
+  const int c4 = N / 4;
+  for (int i = 0; i < nseg; ++i) {
+    const long long r0 = seg_meta[1 + i];
+    const int rows = seg_meta[1 + E + i];
+    const long long n = (long long)((rows + tile_m - 1) / tile_m) * tile_m * c4;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+      const long long row = r0 + p / c4;
+      const int c = (int)(p % c4) * 4;
+      const float* src = part + row * N + c;
+      float4 acc = *reinterpret_cast<const float4*>(src);
+      for (int sl = 1; sl < S; ++sl) {
+        const float4 v = *reinterpret_cast<const float4*>(src + sl * part_stride);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      uint2 o;
+      o.x = pack_bf16x2(acc.x, acc.y);
+      o.y = pack_bf16x2(acc.z, acc.w);
+      *reinterpret_cast<uint2*>(D + row * ldd + c) = o;
+    }
+  }
+}
+
+cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
+                                 int N, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s) {
+  k_splitk_reduce<<<2 * num_sms, 256, 0, s>>>(part, part_stride, S, seg_meta, E, N, 128 * cg, D, ldd);
+  return cudaGetLastError();
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {

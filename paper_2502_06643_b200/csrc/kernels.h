@@ -127,7 +127,12 @@ int pack_block(int F);
 // small token counts); must match the segment padding of the dispatch layout.
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
-                                unsigned* sched, const FusedRet& fr, cudaStream_t s);
+                                unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit = 1,
+                                float* part = nullptr, long long part_stride = 0);
+// ksplit > 1 (plain GEMMs, no fused combine): fp32 partials of the K slices go to
+// part[slice][row][N]; launch_splitk_reduce then writes D = bf16(sum over slices).
+cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
+                                 int N, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.

@@ -64,6 +64,9 @@ struct moe_ctx {
   const void* tmB1_ptr = nullptr;
   const void* tmB2_ptr = nullptr;
   int tmB_nw = -1;
+  // split-K workspace for K6 in decode-sized contexts (fp32 partials [S][cap][H])
+  float* splitk_ws = nullptr;
+  size_t splitk_bytes = 0;
 
   // optional K5/K6 timing event records (3 events per moe_expert_ffn call)
   std::vector<cudaEvent_t> ev;
@@ -555,7 +558,7 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
                  ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
                  ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
                  ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
-                 ctx->item_of_slot, ctx->done_rows, ctx->push_work, ctx->epoch_dev};
+                 ctx->item_of_slot, ctx->done_rows, ctx->push_work, ctx->epoch_dev, ctx->splitk_ws};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -859,10 +862,39 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (rec) CU(cudaEventRecord(ev[1], s));
   tl_rec(ctx, 5, s);
+  // Split-K for K6 in decode-sized contexts: with ~one 128-row M tile per hosted
+  // expert K6 has only n_w x H/256 output tiles (32 for 2 experts at H = 4096), so
+  // most SMs would idle while 32 stream W2.  Split F into S slices until the tiles
+  // cover the SMs; fp32 partials + an ordered reduction (deterministic).
+  int ksplit = 1;
+  if (ctx->gemm_cg == 1 && !vslices && !ctx->ffn_fused) {
+    const long long tiles = (long long)nw * (H / gemm_block_n(H, false));
+    const int nkb = F / 64;
+    while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
+    if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
+  }
+  if (ksplit > 1) {
+    const size_t need = (size_t)ksplit * ctx->cap_rows * H * sizeof(float);
+    if (need > ctx->splitk_bytes) {
+      if (ctx->splitk_ws) CU(cudaFree(ctx->splitk_ws));
+      ctx->splitk_ws = nullptr;
+      ctx->splitk_bytes = 0;
+      CU(cudaMalloc((void**)&ctx->splitk_ws, need));
+      ctx->splitk_bytes = need;
+    }
+  }
   if (!vslices) {
+    const long long pstride = (long long)ctx->cap_rows * H;
     e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
-                            ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s);
+                            ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s, ksplit,
+                            ctx->splitk_ws, pstride);
     if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
+    if (ksplit > 1) {
+      e = launch_splitk_reduce(ctx->splitk_ws, pstride, ksplit, ctx->seg_meta, ctx->E, H, ctx->gemm_cg, ctx->ybuf, H,
+                               ctx->num_sms, s);
+      if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "split-K reduce launch: %s", cudaGetErrorString(e));
+      ctx->launches += 1;
+    }
   } else {
     // partial output of FFN slice q (h columns and W2 columns [q F/tp, (q+1) F/tp))
     // into expert-output buffer q; the combine sums the slices

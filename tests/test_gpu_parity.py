@@ -327,3 +327,18 @@ def test_timeline_events_ordered(cuda_ok):
         assert r[0] == 0.0 and all(v >= 0 for v in r)
         main = [r[0], r[1], r[2], r[4], r[5], r[6], r[7]]   # events on the caller's stream
         assert all(b >= a for a, b in zip(main, main[1:]))
+
+
+@pytest.mark.parametrize("ksplit", ["1", "3", "8"])
+def test_decode_splitk(cuda_ok, ksplit, monkeypatch):
+    """Decode-sized contexts split K6 over F (fp32 partials, ordered reduction);
+    forced slice counts, including slices of a single k-block, against the oracle."""
+    monkeypatch.setenv("MOE_GEMM_CG", "1")
+    monkeypatch.setenv("MOE_DECODE_SPLITK", ksplit)
+    T, H, F, E, k, G = 301, 256, 512, 8, 2, 2
+    P = [1, 0, 1, 1, 0, 1, 0, 1]
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=37)
+    lay = make_layer(T, H, F, E, k, G)
+    out, idx, w = run_layer(lay, inp, P, G)
+    ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    assert_close_layer(bf16_to_f64(out), ref)
