@@ -866,11 +866,16 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // expert K6 has only n_w x H/256 output tiles (32 for 2 experts at H = 4096), so
   // most SMs would idle while 32 stream W2.  Split F into S slices until the tiles
   // cover the SMs; fp32 partials + an ordered reduction (deterministic).
+  // Measured (graph replays, Mixtral layer, profiles/r1_v15_small_t_splitk_*): 4 GPUs
+  // (32 K6 tiles) 64 tokens 0.273 -> 0.252 ms, 256 tokens 0.293 -> 0.283 ms; 2 GPUs
+  // (64 tiles) no gain; 1 GPU (128 tiles) slower (the partials' extra traffic) --
+  // so only grids below a quarter of the SMs are split.
   int ksplit = 1;
   if (ctx->gemm_cg == 1 && !vslices && !ctx->ffn_fused) {
     const long long tiles = (long long)nw * (H / gemm_block_n(H, false));
     const int nkb = F / 64;
-    while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
+    if (tiles * 4 < ctx->num_sms)
+      while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
     if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
   }
   if (ksplit > 1) {
