@@ -681,6 +681,50 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__
   }
 }
 
+// Split-K reduction of the gate/up GEMM (K5): the packed columns of block b are
+// [b*2B, b*2B+B) gate and [b*2B+B, b*2B+2B) up (B = BN/2, moe_pack_w13); the slice
+// sums feed the same SwiGLU as K5's epilogue: h = bf16(silu(g) * u).
+__global__ void __launch_bounds__(256) k_splitk_reduce_swiglu(const float* __restrict__ part, long long part_stride,
+                                                              int S, const int32_t* __restrict__ seg_meta, int E,
+                                                              int F, int B, int tile_m, uint16_t* __restrict__ D,
+                                                              int ldd) {
+  const int nseg = seg_meta[0];
+  const int f4 = F / 4;
+  const int N = 2 * F;
+  for (int i = 0; i < nseg; ++i) {
+    const long long r0 = seg_meta[1 + i];
+    const int rows = seg_meta[1 + E + i];
+    const long long n = (long long)((rows + tile_m - 1) / tile_m) * tile_m * f4;
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+      const long long row = r0 + p / f4;
+      const int f = (int)(p % f4) * 4;
+      const int gc = (f / B) * 2 * B + f % B;
+      const float* src = part + row * N + gc;
+      float4 g = *reinterpret_cast<const float4*>(src);
+      float4 u = *reinterpret_cast<const float4*>(src + B);
+      for (int sl = 1; sl < S; ++sl) {
+        const float4 a = *reinterpret_cast<const float4*>(src + sl * part_stride);
+        const float4 b = *reinterpret_cast<const float4*>(src + sl * part_stride + B);
+        g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
+        u.x += b.x; u.y += b.y; u.z += b.z; u.w += b.w;
+      }
+      const float h0 = g.x / (1.0f + __expf(-g.x)) * u.x, h1 = g.y / (1.0f + __expf(-g.y)) * u.y;
+      const float h2 = g.z / (1.0f + __expf(-g.z)) * u.z, h3 = g.w / (1.0f + __expf(-g.w)) * u.w;
+      uint2 o;
+      o.x = pack_bf16x2(h0, h1);
+      o.y = pack_bf16x2(h2, h3);
+      *reinterpret_cast<uint2*>(D + row * ldd + f) = o;
+    }
+  }
+}
+
+cudaError_t launch_splitk_reduce_swiglu(const float* part, long long part_stride, int S, const int32_t* seg_meta,
+                                        int E, int F, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s) {
+  const int B = gemm_block_n(2 * F, true) / 2;
+  k_splitk_reduce_swiglu<<<2 * num_sms, 256, 0, s>>>(part, part_stride, S, seg_meta, E, F, B, 128 * cg, D, ldd);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
                                  int N, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s) {
   k_splitk_reduce<<<2 * num_sms, 256, 0, s>>>(part, part_stride, S, seg_meta, E, N, 128 * cg, D, ldd);

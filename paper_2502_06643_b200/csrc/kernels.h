@@ -133,6 +133,9 @@ cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, i
 // part[slice][row][N]; launch_splitk_reduce then writes D = bf16(sum over slices).
 cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
                                  int N, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s);
+// Same for the gate/up GEMM: h = bf16(silu(sum gate) * (sum up)), packed columns.
+cudaError_t launch_splitk_reduce_swiglu(const float* part, long long part_stride, int S, const int32_t* seg_meta,
+                                        int E, int F, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.

@@ -856,30 +856,30 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // source rank's return buffer at the item's send-order slot -- the combine
   // all-to-all overlaps the expert GEMM tile by tile
   const FusedRet fused{ctx->ret_table, ctx->seg_src, ctx->G, ctx->ffn_fused ? 1 : 0};
-  cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
-                                      ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
-                                      s);
-  if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
-  if (rec) CU(cudaEventRecord(ev[1], s));
-  tl_rec(ctx, 5, s);
-  // Split-K for K6 in decode-sized contexts: with ~one 128-row M tile per hosted
-  // expert K6 has only n_w x H/256 output tiles (32 for 2 experts at H = 4096), so
-  // most SMs would idle while 32 stream W2.  Split F into S slices until the tiles
-  // cover the SMs; fp32 partials + an ordered reduction (deterministic).
-  // Measured (graph replays, Mixtral layer, profiles/r1_v15_small_t_splitk_*): 4 GPUs
-  // (32 K6 tiles) 64 tokens 0.273 -> 0.252 ms, 256 tokens 0.293 -> 0.283 ms; 2 GPUs
-  // (64 tiles) no gain; 1 GPU (128 tiles) slower (the partials' extra traffic) --
-  // so only grids below a quarter of the SMs are split.
-  int ksplit = 1;
-  if (ctx->gemm_cg == 1 && !vslices && !ctx->ffn_fused) {
-    const long long tiles = (long long)nw * (H / gemm_block_n(H, false));
-    const int nkb = F / 64;
-    if (tiles * 4 < ctx->num_sms)
-      while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
-    if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
+  // Split-K in decode-sized contexts (about one 128-row M tile per hosted expert):
+  // when a GEMM's output tiles cannot cover the SMs, split K into S slices (fp32
+  // partials in a workspace, ordered reduction -- deterministic).  Measured (graph
+  // replays, Mixtral layer, profiles/r1_v15_small_t_splitk_*): K6 at 4 GPUs (32
+  // tiles) 64 tokens 0.273 -> 0.252 ms, 256 tokens 0.293 -> 0.283 ms; no gain at 2
+  // GPUs (64 tiles) and a loss at 1 GPU (128 tiles: the partials' extra traffic), so
+  // only grids below a quarter of the SMs are split.  K5 (SwiGLU applied in the
+  // reduction) is split in two when its grid is under two waves (MOE_DECODE_SPLITK5).
+  int ksplit = 1, ksplit5 = 1;
+  if (ctx->gemm_cg == 1 && !vslices) {
+    if (!ctx->ffn_fused) {
+      const long long tiles = (long long)nw * (H / gemm_block_n(H, false));
+      const int nkb = F / 64;
+      if (tiles * 4 < ctx->num_sms)
+        while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
+      if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
+    }
+    const long long tiles5 = (long long)nw * (2 * F / gemm_block_n(2 * F, true));
+    if (tiles5 < 2 * ctx->num_sms && H / 64 >= 8) ksplit5 = 2;
+    if (const char* env = getenv("MOE_DECODE_SPLITK5")) ksplit5 = std::max(1, atoi(env));
   }
-  if (ksplit > 1) {
-    const size_t need = (size_t)ksplit * ctx->cap_rows * H * sizeof(float);
+  if (ksplit > 1 || ksplit5 > 1) {
+    const size_t need = std::max((size_t)ksplit * ctx->cap_rows * H, (size_t)ksplit5 * ctx->cap_rows * 2 * F) *
+                        sizeof(float);
     if (need > ctx->splitk_bytes) {
       if (ctx->splitk_ws) CU(cudaFree(ctx->splitk_ws));
       ctx->splitk_ws = nullptr;
@@ -888,6 +888,19 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
       ctx->splitk_bytes = need;
     }
   }
+  const long long pstride5 = (long long)ctx->cap_rows * 2 * F;
+  cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
+                                      ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
+                                      s, ksplit5, ctx->splitk_ws, pstride5);
+  if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
+  if (ksplit5 > 1) {
+    e = launch_splitk_reduce_swiglu(ctx->splitk_ws, pstride5, ksplit5, ctx->seg_meta, ctx->E, F, ctx->gemm_cg,
+                                    ctx->hbuf, F, ctx->num_sms, s);
+    if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "split-K SwiGLU reduce launch: %s", cudaGetErrorString(e));
+    ctx->launches += 1;
+  }
+  if (rec) CU(cudaEventRecord(ev[1], s));
+  tl_rec(ctx, 5, s);
   if (!vslices) {
     const long long pstride = (long long)ctx->cap_rows * H;
     e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,

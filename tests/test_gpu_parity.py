@@ -329,12 +329,14 @@ def test_timeline_events_ordered(cuda_ok):
         assert all(b >= a for a, b in zip(main, main[1:]))
 
 
-@pytest.mark.parametrize("ksplit", ["1", "3", "8"])
-def test_decode_splitk(cuda_ok, ksplit, monkeypatch):
-    """Decode-sized contexts split K6 over F (fp32 partials, ordered reduction);
-    forced slice counts, including slices of a single k-block, against the oracle."""
+@pytest.mark.parametrize("ksplit,ksplit5", [("1", "1"), ("3", "2"), ("8", "4")])
+def test_decode_splitk(cuda_ok, ksplit, ksplit5, monkeypatch):
+    """Decode-sized contexts split K6 over F and K5 over H (fp32 partials, ordered
+    reduction; K5's SwiGLU applied in the reduction); forced slice counts,
+    including slices of a single k-block, against the oracle."""
     monkeypatch.setenv("MOE_GEMM_CG", "1")
     monkeypatch.setenv("MOE_DECODE_SPLITK", ksplit)
+    monkeypatch.setenv("MOE_DECODE_SPLITK5", ksplit5)
     T, H, F, E, k, G = 301, 256, 512, 8, 2, 2
     P = [1, 0, 1, 1, 0, 1, 0, 1]
     inp = Inputs(T, H, F, E, k, s=1.6, seed=37)
