@@ -862,8 +862,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // replays, Mixtral layer, profiles/r1_v15_small_t_splitk_*): K6 at 4 GPUs (32
   // tiles) 64 tokens 0.273 -> 0.252 ms, 256 tokens 0.293 -> 0.283 ms; no gain at 2
   // GPUs (64 tiles) and a loss at 1 GPU (128 tiles: the partials' extra traffic), so
-  // only grids below a quarter of the SMs are split.  K5 (SwiGLU applied in the
-  // reduction) is split in two when its grid is under two waves (MOE_DECODE_SPLITK5).
+  // only grids below a quarter of the SMs are split.
   int ksplit = 1, ksplit5 = 1;
   if (ctx->gemm_cg == 1 && !vslices) {
     if (!ctx->ffn_fused) {
@@ -873,8 +872,8 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
         while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
       if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
     }
-    const long long tiles5 = (long long)nw * (2 * F / gemm_block_n(2 * F, true));
-    if (tiles5 < 2 * ctx->num_sms && H / 64 >= 8) ksplit5 = 2;
+    // K5 split-K is available (MOE_DECODE_SPLITK5=S) but off: measured slower at
+    // 2 and 4 GPUs (4 GPUs 64 tokens 0.246 -> 0.264 ms, profiles/r1_v15_small_t_k5split_*)
     if (const char* env = getenv("MOE_DECODE_SPLITK5")) ksplit5 = std::max(1, atoi(env));
   }
   if (ksplit > 1 || ksplit5 > 1) {
