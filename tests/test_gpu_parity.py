@@ -266,6 +266,42 @@ def test_mixtral_layer_full_size_sampled(cuda_ok):
     assert_close_layer(bf16_to_f64(out[sel]), ref)
 
 
+def test_e64_layer_full_size_sampled(cuda_ok):
+    """BASELINE configs[4] shape (E64 top-8, H4096, F2048, T = 65536) over 4
+    virtual EP ranks with the ILP-1 balanced placement, checked on sampled tokens
+    against the oracle's direct definition (each sampled token touches 8 experts)."""
+    from paper_2502_06643_b200 import placement
+    T, H, F, E, k, G = 65536, 4096, 2048, 64, 8, 4
+    dev = torch.device(DEV)
+    x = synth.hidden_states(T, H, seed=0, device=dev)
+    logits = synth.zipf_logits(T, E, 1.6, seed=0, device=dev)
+    ws = [synth.expert_weights(e, H, F, 0, device=dev) for e in range(E)]
+    moe = _moe()
+    lay = make_layer(T, H, F, E, k, G)
+    idx, w = lay.route(logits, k)
+    load = np.bincount(idx.cpu().numpy().ravel(), minlength=E)
+    P = placement.balanced(load, G)
+    lay.dispatch(x, idx, P)
+    w13 = moe.pack_w13(torch.stack([q[0] for q in ws]), torch.stack([q[1] for q in ws]))
+    w2 = torch.stack([q[2] for q in ws])
+    lay.expert_ffn(w13, w2)
+    out = lay.combine(w)
+    lay.sync()
+    sel = np.array(sorted(set(np.random.default_rng(1).integers(0, T, 40).tolist()) | {0, T - 1}))
+    xs = bf16_to_f64(x[sel])
+    ls = logits[sel].cpu().numpy()
+    cache = {}
+
+    def fn(e, rows):
+        if e not in cache:
+            cache[e] = tuple(bf16_to_f64(m) for m in ws[e])
+        from oracle import ffn
+        return ffn.swiglu(rows, *cache[e])[1]
+    ref, ridx, rw = olayer.layer_direct(xs, ls, k, fn)
+    assert np.array_equal(idx[sel].cpu().numpy(), ridx)
+    assert_close_layer(bf16_to_f64(out[sel]), ref)
+
+
 def test_cuda_graph_replay_bit_exact(cuda_ok):
     """A whole layer (route .. combine) captured in a CUDA graph replays to the
     eager result bit-exactly (no host round trip on the path; moe.h)."""

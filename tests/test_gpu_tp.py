@@ -109,6 +109,26 @@ def test_tp_layer_parity(cuda_ok, T, H, F, E, k, G, tp, P):
     assert_close_layer(bf16_to_f64(out), direct)
 
 
+def test_tp_decode_tiles(cuda_ok, monkeypatch):
+    """TP with 128-row GEMM tiles on one CTA (decode-sized contexts)."""
+    monkeypatch.setenv("MOE_GEMM_CG", "1")
+    T, H, F, E, k, G, tp = 333, 128, 512, 8, 2, 2, 2
+    P = [0, 1, 1, 0, 1, 0, 0, 1]
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=41)
+    lay = make_layer(T, H, F, E, k, G, tp)
+    moe = _moe()
+    x, logits = inp.to_device(DEV)
+    idx, w = lay.route(logits, k)
+    lay.dispatch(x, idx, P)
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E)))
+    lay.expert_ffn(moe.pack_w13(w1, w3), w2)
+    out = lay.combine(w)
+    lay.sync()
+    ref, _, _, _ = olayer.layer_ep_tp(bf16_to_f64(inp.x), inp.logits.numpy(), k, np.array(P), G, tp,
+                                      inp.oracle_tp_fn(tp))
+    assert_close_layer(bf16_to_f64(out), ref)
+
+
 def test_tp_bad_configs(cuda_ok):
     moe = _moe()
     kw = dict(max_tokens=64, hidden=64, num_experts=8, max_k=2)
