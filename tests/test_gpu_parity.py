@@ -294,6 +294,7 @@ def test_e64_layer_full_size_sampled(cuda_ok):
 
     def fn(e, rows):
         if e not in cache:
+            cache.clear()                 # layer_direct visits each expert once
             cache[e] = tuple(bf16_to_f64(m) for m in ws[e])
         from oracle import ffn
         return ffn.swiglu(rows, *cache[e])[1]
