@@ -64,5 +64,7 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas-v", action="store_true")
+    ap.add_argument("--define", action="append", default=[], help="extra -D macro (A/B experiments)")
     a = ap.parse_args()
-    print(build(force=a.force or a.ptxas_v, verbose=a.verbose, extra=["-Xptxas", "-v"] if a.ptxas_v else []))
+    extra = (["-Xptxas", "-v"] if a.ptxas_v else []) + ["-D" + d for d in a.define]
+    print(build(force=a.force or bool(extra), verbose=a.verbose, extra=extra))
