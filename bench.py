@@ -431,18 +431,37 @@ def run_ours(args):
                 # load of layer l-1 and co-activation l-1 -> l in one pass
                 lay.route_stats(idx_l[li - 1], idx_l[li], load_l[li - 1], coact_l[li - 1])
         lay.route_stats(idx_l[L - 1], None, load_l[L - 1], None)
-        for li in range(L):
-            lay.stats_allreduce(load_l[li], coact_l[li] if li < L - 1 else None)
+        lay.stats_allreduce_layers(load_l, coact_l)      # one collective for the whole pass
+
+    def time_region(fn):
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        fn()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        return float(max_over_ranks([s0.elapsed_time(s1)])[0])
 
     stats_pass_timed()
-    barrier()
-    torch.cuda.synchronize()
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record(stream)
-    stats_pass_timed()
-    s1.record(stream)
-    torch.cuda.synchronize()
-    stats_ms = float(max_over_ranks([s0.elapsed_time(s1)])[0])
+    stats_ms = time_region(stats_pass_timed)
+    # the same pass captured once in a CUDA graph (route, stats and the NCCL
+    # all-reduce replay without host launches)
+    stats_graph_ms = None
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            stats_pass_timed()
+        stream.wait_stream(side)
+        sg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(sg):
+            stats_pass_timed()
+        sg.replay()
+        stats_graph_ms = time_region(sg.replay)
+        del sg
+    except Exception as ex:  # graph capture is a measurement variant only
+        print(f"stats-pass graph capture skipped: {ex}", file=sys.stderr)
 
     # ---- end-to-end through the public API with host buffers (headline placement)
     head = "contiguous" if "contiguous" in placements else next(iter(placements))
@@ -540,8 +559,11 @@ def run_ours(args):
             "clocks": r["clocks"],
             "placements": {n: {kk: v for kk, v in res.items() if kk not in ("clocks",)} for n, res in results.items()},
             "stats_pass": {"layers": L, "tokens_total": T, "ms": stats_ms, "us_per_layer": stats_ms * 1e3 / L,
+                           "graph_ms": stats_graph_ms,
+                           "graph_us_per_layer": stats_graph_ms * 1e3 / L if stats_graph_ms else None,
                            "what": "moe_route + moe_route_stats per layer (load and l-1 -> l co-activation), "
-                                   "then moe_stats_allreduce; synth.multilayer_logits (dependency 0.5)"},
+                                   "then one moe_stats_allreduce_layers; synth.multilayer_logits (dependency "
+                                   "0.5); eager launches and one CUDA-graph replay"},
         }
         if N == 1 and not args.no_cpu_baseline:
             with host_threads():

@@ -145,6 +145,12 @@ moe_status moe_route_stats(moe_ctx_t ctx, const int32_t* idx_l, const int32_t* i
 moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E,
                                moe_stream_t stream);
 
+/* The same for a whole profiling pass in one collective: load int64 [L][E] and
+ * coact int64 [L-1][E][E] (coact may be NULL; L >= 1), e.g. the per-layer
+ * statistics of moe_route_stats over L layers (P:L581 P_{e,l}, P:L654 R_{e1,e2,l}). */
+moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E, int32_t L,
+                                      moe_stream_t stream);
+
 /* ---- a3-a5: dispatch (G7, G8, G9, G13, G14) ---
  * x: bf16 [T][H] (this process's tokens); idx: int32 [T][k] from moe_route.
  * expert_to_rank: HOST int32 [E], values in [0, G/tp) (the placement input: the

@@ -636,6 +636,20 @@ moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int
   return MOE_OK;
 }
 
+moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E, int32_t L,
+                                      moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (E != ctx->E || !load || L < 1) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  ctx->last_stream = s;
+  if (!ctx->comm) return MOE_OK;
+  NC(ncclGroupStart());
+  NC(ncclAllReduce(load, load, (size_t)L * E, ncclInt64, ncclSum, ctx->comm, s));
+  if (coact && L > 1) NC(ncclAllReduce(coact, coact, (size_t)(L - 1) * E * E, ncclInt64, ncclSum, ctx->comm, s));
+  NC(ncclGroupEnd());
+  return MOE_OK;
+}
+
 moe_status moe_pack_w13(const moe_bf16* w1, const moe_bf16* w3, int32_t n, int32_t F, int32_t H, moe_bf16* w13,
                         moe_stream_t stream) {
   moe_ctx_t ctx = nullptr;

@@ -22,7 +22,7 @@ STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_CUDA", 3: "MOE_ERR_
 
 # Every symbol include/moe.h declares (checked by tests/test_abi_cpu.py).
 EXPORTS = ["moe_get_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_sync", "moe_status_str",
-           "moe_last_error", "moe_abi_version", "moe_route", "moe_route_stats", "moe_stats_allreduce",
+           "moe_last_error", "moe_abi_version", "moe_route", "moe_route_stats", "moe_stats_allreduce", "moe_stats_allreduce_layers",
            "moe_dispatch", "moe_expert_ffn", "moe_combine", "moe_pack_w13", "moe_placement_contiguous",
            "moe_layout_host", "moe_debug_plan", "moe_debug_identity_ffn", "moe_debug_recv", "moe_kernel_launches",
            "moe_ffn_timing_enable", "moe_ffn_timing_read", "moe_timeline_enable", "moe_timeline_read"]
@@ -60,6 +60,7 @@ def load_library(path=LIB_PATH):
         "moe_route": [P, P, I32, I32, I32, P, P, P],
         "moe_route_stats": [P, P, P, I32, I32, I32, P, P, P],
         "moe_stats_allreduce": [P, P, P, I32, P],
+        "moe_stats_allreduce_layers": [P, P, P, I32, I32, P],
         "moe_dispatch": [P, P, P, I32, I32, P, P, P],
         "moe_expert_ffn": [P, P, P, P],
         "moe_combine": [P, P, P, P],
@@ -252,6 +253,11 @@ class MoeLayer:
 
     def stats_allreduce(self, load, coact, stream=None):
         self._c(_lib.moe_stats_allreduce(self._ctx, _ptr(load), _ptr(coact), self.E, _stream(stream)))
+
+    def stats_allreduce_layers(self, load, coact, stream=None):
+        """load int64 [L][E], coact int64 [L-1][E][E] (or None): one collective."""
+        L = load.shape[0]
+        self._c(_lib.moe_stats_allreduce_layers(self._ctx, _ptr(load), _ptr(coact), self.E, L, _stream(stream)))
 
     # a3-a5
     def dispatch(self, x, idx, expert_to_rank, info=False, stream=None):

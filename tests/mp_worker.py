@@ -106,6 +106,25 @@ def main():
     lay.stats_allreduce(load, None)
     lay.sync()
     assert np.array_equal(load.cpu().numpy(), np.bincount(ridx.ravel(), minlength=E))
+    # a multi-layer pass in one collective: per-layer loads and layer-pair co-activation
+    L3 = 3
+    loads = torch.zeros(L3, E, dtype=torch.int64, device=dev)
+    coacts = torch.zeros(L3 - 1, E, E, dtype=torch.int64, device=dev)
+    lg = [logits, logits.flip(1).contiguous(), logits.roll(1, 1).contiguous()]
+    ids = [lay.route(q, k)[0] for q in lg]
+    for li in range(L3):
+        lay.route_stats(ids[li], ids[li + 1] if li + 1 < L3 else None, loads[li],
+                        coacts[li] if li + 1 < L3 else None)
+    lay.stats_allreduce_layers(loads, coacts)
+    lay.sync()
+    lga = [inp.logits.numpy(), inp.logits.numpy()[:, ::-1].copy(), np.roll(inp.logits.numpy(), 1, 1)]
+    rids = [oroute.route(q, k)[0] for q in lga]
+    from oracle import stats as ostats
+    for li in range(L3):
+        assert np.array_equal(loads[li].cpu().numpy(), ostats.load_counts(rids[li], E)), "multi-layer load"
+        if li + 1 < L3:
+            assert np.array_equal(coacts[li].cpu().numpy(), ostats.coactivation_counts(rids[li], rids[li + 1], E)), \
+                "multi-layer co-activation"
 
     # CUDA-graph capture of a P2P layer: the flags carry a device-side epoch, so
     # replays of the captured layer match the eager result bit-exactly
