@@ -893,7 +893,13 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (ksplit > 1 || ksplit5 > 1) {
     const size_t need = std::max((size_t)ksplit * ctx->cap_rows * H, (size_t)ksplit5 * ctx->cap_rows * 2 * F) *
                         sizeof(float);
-    if (need > ctx->splitk_bytes) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(s, &cs));
+    if (need > ctx->splitk_bytes && cs != cudaStreamCaptureStatusNone) {
+      // no allocation inside a CUDA-graph capture: run this launch unsplit (an eager
+      // call before the capture sizes the workspace)
+      ksplit = ksplit5 = 1;
+    } else if (need > ctx->splitk_bytes) {
       if (ctx->splitk_ws) CU(cudaFree(ctx->splitk_ws));
       ctx->splitk_ws = nullptr;
       ctx->splitk_bytes = 0;
