@@ -73,7 +73,7 @@ typedef struct {
   int32_t max_tokens;     /* upper bound on T of any call (per process) */
   int32_t hidden;         /* H; multiple of 64 */
   int32_t ffn;            /* F; multiple of 64 */
-  int32_t num_experts;    /* E; 1..256 (route_stats: E <= 128) */
+  int32_t num_experts;    /* E; 1..256 */
   int32_t max_k;          /* upper bound on k; 1..E, <= 16 */
   int32_t world;          /* real EP ranks (processes); 1 => no NCCL */
   int32_t rank;           /* this process's rank in [0, world) */

@@ -611,7 +611,6 @@ moe_status moe_route_stats(moe_ctx_t ctx, const int32_t* idx_l, const int32_t* i
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
   if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
   if (E != ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "E=%d != context E=%d", E, ctx->E);
-  if (E > 128) return fail(ctx, MOE_ERR_UNSUPPORTED, "route_stats supports E <= 128");
   if (k < 1 || k > E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
   if (T > 0 && (!idx_l || !load)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
   if (idx_l1 && !coact) return fail(ctx, MOE_ERR_INVALID_ARG, "coact is NULL but idx_l1 is given");

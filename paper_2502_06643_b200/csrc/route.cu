@@ -94,15 +94,18 @@ void launch_route(const float* logits, int T, int E, int k, int32_t* idx, float*
 
 // ------------------------------------------------------------------------ K9
 // Shared-memory histograms (load [E], coact [E][E]) with warp-aggregated
-// increments (__match_any_sync), flushed to int64 global counters.
+// increments (__match_any_sync), flushed to int64 global counters.  For E > 128
+// the E x E co-activation histogram does not fit in shared memory: its
+// (warp-aggregated) increments go straight to the int64 global counters.
 __global__ void __launch_bounds__(256) k_route_stats(const int32_t* __restrict__ idx_l,
                                                      const int32_t* __restrict__ idx_l1, int T, int E, int k,
                                                      unsigned long long* __restrict__ load,
-                                                     unsigned long long* __restrict__ coact, int* err) {
-  extern __shared__ int hist[];  // [E] load, then [E*E] coact
+                                                     unsigned long long* __restrict__ coact, int* err,
+                                                     int smem_co) {
+  extern __shared__ int hist[];  // [E] load, then [E*E] coact (smem_co)
   int* hload = hist;
   int* hco = hist + E;
-  const int nbins = E + (idx_l1 ? E * E : 0);
+  const int nbins = E + (idx_l1 && smem_co ? E * E : 0);
   for (int b = threadIdx.x; b < nbins; b += blockDim.x) hist[b] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -126,7 +129,10 @@ __global__ void __launch_bounds__(256) k_route_stats(const int32_t* __restrict__
           }
           int bin = (e1 >= 0 && e2 >= 0) ? e1 * E + e2 : -1;
           unsigned m2 = __match_any_sync(0xffffffffu, bin);
-          if (bin >= 0 && lane == __ffs(m2) - 1) atomicAdd(&hco[bin], __popc(m2));
+          if (bin >= 0 && lane == __ffs(m2) - 1) {
+            if (smem_co) atomicAdd(&hco[bin], __popc(m2));
+            else atomicAdd(&coact[bin], (unsigned long long)__popc(m2));
+          }
         }
       }
     }
@@ -147,14 +153,15 @@ void launch_route_stats(const int32_t* idx_l, const int32_t* idx_l1, int T, int 
   const int threads = 256;
   int blocks = (T + threads - 1) / threads;
   if (blocks > 2 * num_sms) blocks = 2 * num_sms;
-  size_t smem = sizeof(int) * (E + (idx_l1 ? E * E : 0));
+  const int smem_co = E <= 128 ? 1 : 0;
+  size_t smem = sizeof(int) * (E + (idx_l1 && smem_co ? E * E : 0));
   static bool attr = false;
   if (!attr) {  // E up to 128 needs > 48 KB for the E x E histogram
     cudaFuncSetAttribute(k_route_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * (128 + 128 * 128)));
     attr = true;
   }
   k_route_stats<<<blocks, threads, smem, s>>>(idx_l, idx_l1, T, E, k, (unsigned long long*)load,
-                                              (unsigned long long*)coact, err);
+                                              (unsigned long long*)coact, err, smem_co);
 }
 
 }  // namespace moe

@@ -61,7 +61,7 @@ def test_route_empty(cuda_ok):
 
 
 # ------------------------------------------------------------------ a2
-@pytest.mark.parametrize("T,E,k", [(5000, 8, 2), (1031, 64, 8), (333, 128, 4), (1, 8, 2)])
+@pytest.mark.parametrize("T,E,k", [(5000, 8, 2), (1031, 64, 8), (333, 128, 4), (1, 8, 2), (777, 256, 16), (300, 200, 3)])
 def test_route_stats_bit_exact(cuda_ok, T, E, k):
     lay = make_layer(T, 64, 64, E, k)
     l0 = synth.zipf_logits(T, E, 1.6, seed=1)
