@@ -182,7 +182,11 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
  *   w13 = moe_pack_w13(W1[:, qF_q:(q+1)F_q, :], W3[same rows], n_w, F_q, H) [n_w][2F_q][H],
  *   w2  = W2[:, :, qF_q:(q+1)F_q] made contiguous                          [n_w][H][F_q];
  * Y is then this slice's bf16 partial output.  tp > 1, virtual ranks: the full
- * w13 / w2 as above; every slice's partial output is computed separately. 
+ * w13 / w2 as above; every slice's partial output is computed separately.
+ * Decode-sized contexts may split the down projection over F (fp32 partials in
+ * a context-owned workspace, summed in a fixed order before the bf16 rounding),
+ * so Y can differ from an unsplit run in the last bf16 bit; the result is
+ * deterministic for a given context.
  * Collective in MOE_A2A_P2P mode: every rank calls it after moe_dispatch, also
  * a rank hosting no expert (w13/w2 may then be NULL) -- it raises the flag the
  * peers' moe_combine waits for. */
