@@ -363,12 +363,41 @@ def run_ours(args):
         total_max = float(max_over_ranks([total])[0])
         rows_here = int(info.recv_rows) if info is not None else 0
         recv_counts = list(info.recv_counts)[:G]
+        # per-placement roofline: the slower of the tensor bound
+        # of the busiest rank (6 H F/tp FLOPs per routed row it computes), its HBM
+        # bound (hosted weights + routed activations) and its NVLink bound (rows
+        # that cross NVLink in dispatch + combine at the measured 770 GB/s)
+        sc = torch.tensor([int(info.send_counts[g]) for g in range(G)], dtype=torch.float64, device=dev)
+        if N > 1:
+            allsc = [torch.zeros_like(sc) for _ in range(N)]
+            dist.all_gather(allsc, sc)
+            send_m = torch.stack(allsc).cpu().numpy()          # [rank][group]
+        else:
+            send_m = sc.cpu().numpy()[None, :]
+        peak_b = peaks.get("bf16_tflops", 1620.5) * 1e12
+        hbm = float(peaks.get("hbm_gbs", peaks.get("hbm_gbps", 6449.1))) * 1e9
+        t_tc = t_hbm = t_nvl = 0.0
+        for r in range(N):
+            g = r // tp
+            rows = float(recv_counts[g])
+            n_exp = int(sum(1 for e in range(E) if P[e] == g))
+            t_tc = max(t_tc, 6.0 * H * Fl * rows / peak_b)
+            t_hbm = max(t_hbm, (n_exp * 3.0 * H * Fl * 2 + rows * (2 * H * 2 + 3 * Fl * 2)) / hbm)
+            out_rows = sum(send_m[r][q] * (tp if q != g else tp - 1) for q in range(G))
+            in_rows = sum(send_m[s_][g] for s_ in range(N) if s_ != r)
+            t_nvl = max(t_nvl, 2.0 * H * max(out_rows, in_rows) / 770e9)
+        roof_ms = max(t_tc, t_hbm, t_nvl) * 1e3
         res = dict(
             total_ms=total_max, ms_per_step=total_max / args.steps,
             p50_ms=float(np.percentile(per_step_max, 50)), p99_ms=float(np.percentile(per_step_max, 99)),
             mean_of_max_ms=float(np.mean(per_step_max)), mean_over_ranks_ms=float(np.mean(per_step_mean)),
             tokens_per_s=T / (total_max / args.steps / 1e3), expert_to_rank=[int(v) for v in P],
             recv_rows_per_rank=recv_counts, clocks=clk, launches=launches,
+            roofline={"ms": roof_ms, "bound": ["tensor", "hbm", "nvlink"][int(np.argmax([t_tc, t_hbm, t_nvl]))],
+                      "tensor_ms": t_tc * 1e3, "hbm_ms": t_hbm * 1e3, "nvlink_ms": t_nvl * 1e3,
+                      "frac": roof_ms / (total_max / args.steps),
+                      "peaks": "bf16 burst (MEASURED_PEAKS.json), HBM copy (MEASURED_PEAKS.json), NVLink 770 GB/s "
+                               "measured peer copy (B200_PROFILING.md)"},
             k5_ms=float(np.mean(k5)) if k5 else None, k6_ms=float(np.mean(k6)) if k6 else None,
             rows_rank0=rows_here)
         # per-phase breakdown (separate, untimed-for-value loop): the paper's
