@@ -191,24 +191,6 @@ __device__ __forceinline__ void tma_load_2d_pair(const void* tmap, uint32_t bar_
       ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(bar_cluster_addr)
       : "memory");
 }
-// TMA gather4: rows r0..r3 (arbitrary) x 64 columns from a 2D map with box {64, 1},
-// landing as 4 consecutive 128-byte rows (swizzled like a box load at that address)
-__device__ __forceinline__ void tma_gather4_2d(const void* tmap, uint64_t* bar, void* smem_dst, int c0, int r0, int r1,
-                                               int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-      "%5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_gather4_2d_pair(const void* tmap, uint32_t bar_cluster_addr, void* smem_dst, int c0,
-                                                    int r0, int r1, int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], "
-      "[%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar_cluster_addr)
-      : "memory");
-}
 __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                uint32_t accumulate) {
   asm volatile(

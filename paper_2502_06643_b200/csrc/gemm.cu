@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
                    int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf,
-                   int tile_ahead, int ksplit, float* __restrict__ part, long long part_stride, int gather_a) {
+                   int tile_ahead, int ksplit, float* __restrict__ part, long long part_stride) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   extern __shared__ uint8_t smem_raw[];
@@ -331,25 +331,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (CG == 2) {
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-            if (gather_a) {  // (experiment) the 128 A rows as 32 gather4 loads
-              uint8_t* dst = smA + stage * C::A_BYTES;
-              for (int g = 0; g < 32; ++g)
-                tma_gather4_2d_pair(&tmA, fb, dst + g * 512, kb * BK, a_row + 4 * g, a_row + 4 * g + 1,
-                                    a_row + 4 * g + 2, a_row + 4 * g + 3);
-            } else {
-              tma_load_2d_pair(&tmA, fb, smA + stage * C::A_BYTES, kb * BK, a_row);
-            }
+            tma_load_2d_pair(&tmA, fb, smA + stage * C::A_BYTES, kb * BK, a_row);
             tma_load_2d_pair(&tmB, fb, smB + stage * C::B_BYTES, kb * BK, b_row);
           } else {
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-            if (gather_a) {
-              uint8_t* dst = smA + stage * C::A_BYTES;
-              for (int g = 0; g < 32; ++g)
-                tma_gather4_2d(&tmA, &full[stage], dst + g * 512, kb * BK, a_row + 4 * g, a_row + 4 * g + 1,
-                               a_row + 4 * g + 2, a_row + 4 * g + 3);
-            } else {
-              tma_load_2d(&tmA, &full[stage], smA + stage * C::A_BYTES, kb * BK, a_row);
-            }
+            tma_load_2d(&tmA, &full[stage], smA + stage * C::A_BYTES, kb * BK, a_row);
             tma_load_2d(&tmB, &full[stage], smB + stage * C::B_BYTES, kb * BK, b_row);
           }
           if (++stage == C::STAGES) {
@@ -584,8 +570,7 @@ int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu)
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const SrcWait& sw, int* err, unsigned* sched,
-                               const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride,
-                               int gather_a) {
+                               const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride) {
   using C = GemmCfg<BN, CG, FUSED>;
   auto kern = k_grouped_gemm<BN, SWIGLU, CG, FUSED>;
   static bool configured = false;
@@ -637,19 +622,19 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
     ahead = (env && atoi(env) != 0) ? 1 : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
-                            sched, fr, pf, ahead, ksplit, part, part_stride, gather_a);
+                            sched, fr, pf, ahead, ksplit, part, part_stride);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
                                 unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit, float* part,
-                                long long part_stride, int gather_a) {
+                                long long part_stride) {
   const int bn = gemm_block_n(N, swiglu);
   if (ksplit < 1) ksplit = 1;
   const bool fused = fr.enabled && !swiglu;
 #define MOE_GO(BN_, SW_, CG_, FU_) \
   launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s, ksplit, part, \
-                                  part_stride, gather_a)
+                                  part_stride)
 #define MOE_GO2(BN_, CG_) (fused ? MOE_GO(BN_, false, CG_, true) : MOE_GO(BN_, false, CG_, false))
   if (cg == 2) {
     if (swiglu) return bn == 256 ? MOE_GO(256, true, 2, false) : MOE_GO(128, true, 2, false);

@@ -128,7 +128,7 @@ int pack_block(int F);
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
                                 unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit = 1,
-                                float* part = nullptr, long long part_stride = 0, int gather_a = 0);
+                                float* part = nullptr, long long part_stride = 0);
 // ksplit > 1 (plain GEMMs, no fused combine): fp32 partials of the K slices go to
 // part[slice][row][N]; launch_splitk_reduce then writes D = bf16(sum over slices).
 cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,

@@ -57,8 +57,6 @@ struct moe_ctx {
   uint16_t* retbuf = nullptr;   // [send_rows][H]
   alignas(64) uint8_t tmA1[128];  // A of GEMM1: recv [cap][H]
   alignas(64) uint8_t tmA2[128];  // A of GEMM2: hbuf [cap][F]
-  alignas(64) uint8_t tmA1g[128];  // (experiment, MOE_K5_GATHER4) recv with box {64, 1} for gather4
-  bool k5_gather = false;
   alignas(64) uint8_t tmB1[128];
   alignas(64) uint8_t tmB2[128];
   alignas(64) uint8_t tmA2s[kMaxTP][128];  // virtual TP: h column slice q
@@ -440,11 +438,6 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   if (!make_tmap_2d(ctx->tmA1, ctx->recv, ctx->cap_rows, c.hidden, 128) ||
       !make_tmap_2d(ctx->tmA2, ctx->hbuf, ctx->cap_rows, ctx->Fl, 128)) {
     fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
-    return bail(MOE_ERR_CUDA);
-  }
-  ctx->k5_gather = getenv("MOE_K5_GATHER4") && atoi(getenv("MOE_K5_GATHER4")) != 0;
-  if (ctx->k5_gather && !make_tmap_2d(ctx->tmA1g, ctx->recv, ctx->cap_rows, c.hidden, 1)) {
-    fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the gather4 map");
     return bail(MOE_ERR_CUDA);
   }
   if (ctx->virt && tp > 1)
@@ -914,10 +907,9 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     }
   }
   const long long pstride5 = (long long)ctx->cap_rows * 2 * F;
-  cudaError_t e = launch_grouped_gemm(ctx->k5_gather ? ctx->tmA1g : ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta,
-                                      ctx->E, 2 * F, H, true, ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev,
-                                      ctx->done_counter + 2, plain, s, ksplit5, ctx->splitk_ws, pstride5,
-                                      ctx->k5_gather ? 1 : 0);
+  cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
+                                      ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
+                                      s, ksplit5, ctx->splitk_ws, pstride5);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (ksplit5 > 1) {
     e = launch_splitk_reduce_swiglu(ctx->splitk_ws, pstride5, ksplit5, ctx->seg_meta, ctx->E, F, ctx->gemm_cg,
