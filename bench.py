@@ -184,7 +184,7 @@ def oracle_time(cfg, n_tok, reps, seed, s, G, P, state=None, tp=1):
     rng = np.random.default_rng(seed + 99)
     times = []
     for _ in range(reps):
-        sel = np.sort(rng.choice(cfg["T"], n_tok, replace=False))
+        sel = np.sort(rng.choice(cfg["T"], min(n_tok, cfg["T"]), replace=False))
         xs = obf.from_bits(x[sel].contiguous().view(torch.int16).numpy().view(np.uint16))
         ls = logits[sel].numpy()
         t0 = time.perf_counter()
@@ -599,9 +599,9 @@ def run_ours(args):
                 times, _ = oracle_time(cfg, args.cpu_tokens, args.cpu_reps, args.seed, s, 1, np.zeros(E, np.int32))
                 cores = threads_used()
             line["cpu_baseline"] = {
-                "value": args.cpu_tokens * len(times) / sum(times), "unit": "tokens/s", "cores": cores,
+                "value": min(args.cpu_tokens, T) * len(times) / sum(times), "unit": "tokens/s", "cores": cores,
                 "kind": "oracle",
-                "sample": f"{args.cpu_reps} x {args.cpu_tokens} random tokens of the same workload through "
+                "sample": f"{args.cpu_reps} x {min(args.cpu_tokens, T)} random tokens of the same workload through "
                           f"oracle.layer.layer_ep (float64 numpy, G=1); weights pre-converted bf16->float64 "
                           f"outside the timed region; total {sum(times):.1f} s"}
         print(json.dumps(line), flush=True)
