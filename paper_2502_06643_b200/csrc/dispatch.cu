@@ -189,9 +189,21 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
       for (int g = 0; g < a.G; ++g) b.peer_sig[g]->cnt[a.me * E + e] = b.cnt_local[e];
       __threadfence_system();
     }
+    // the placement this rank dispatches with travels with its counts: every rank
+    // checks that all ranks agree (the call discipline of moe_dispatch)
+    __shared__ unsigned my_hash;
+    if (threadIdx.x == 0) {
+      unsigned h = 2166136261u;  // FNV-1a over the placement
+      for (int q = 0; q < E; ++q) h = (h ^ (unsigned)b.P[q]) * 16777619u;
+      my_hash = h;
+      for (int g = 0; g < a.G; ++g) b.peer_sig[g]->phash[a.me] = h;
+      __threadfence_system();
+    }
     __syncthreads();
     if (threadIdx.x == 0) signal_all(a, b, 0);
     wait_flags_geq(b.my_sig->flag_cnt, a.G, cur_epoch(a.epoch_ptr), b.err);
+    for (int g = threadIdx.x; g < a.G; g += blockDim.x)
+      if (((volatile unsigned*)b.my_sig->phash)[g] != my_hash) atomicOr(b.err, kErrPlacement);
     cnt = b.my_sig->cnt;
   }
   if (e < E) {

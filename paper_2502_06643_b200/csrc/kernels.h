@@ -17,6 +17,7 @@ struct SigBlock {
   unsigned flag_cnt[64];      // flag_cnt[s] = epoch once source s's count row landed
   unsigned flag_data[64];     // flag_data[s] = epoch once every row s sends here landed
   unsigned flag_y[64];        // flag_y[g] = epoch once rank g's expert outputs are ready
+  unsigned phash[64];         // phash[s] = hash of the placement source s dispatched with
   unsigned flag_seg[64][256]; // flag_seg[s][pos] = epoch once source s's rows of this rank's
                               // pos-th hosted expert landed (slot-ordered push, k_push)
 };

@@ -576,10 +576,11 @@ static moe_status check_device_error(moe_ctx_t ctx) {
   CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   if (e) {
     cudaMemset(ctx->err_dev, 0, sizeof(int));
-    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s",
+    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s",
                 (e & kErrBadExpert) ? " expert id out of range" : "",
                 (e & kErrCapacity) ? " receive capacity exceeded" : "",
-                (e & kErrTimeout) ? " P2P peer flag timeout (a rank skipped a collective call?)" : "");
+                (e & kErrTimeout) ? " P2P peer flag timeout (a rank skipped a collective call?)" : "",
+                (e & kErrPlacement) ? " ranks dispatched with different expert_to_rank maps" : "");
   }
   return MOE_OK;
 }
