@@ -161,9 +161,10 @@ moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coa
  * hosting its expert.  Collective when world > 1 (NCCL mode synchronises the
  * stream once to read the G x E count matrix).  The plan stays in the context
  * until the next moe_dispatch.  info: host, optional; if non-NULL the call
- * synchronises `stream` and fills it.  MOE_A2A_P2P: a hash of expert_to_rank
- * travels with the counts and every rank checks that all ranks dispatched with
- * the same placement (a mismatch latches MOE_ERR_DEVICE).
+ * synchronises `stream` and fills it.  A hash of expert_to_rank travels with the
+ * counts and every rank checks that all ranks dispatched with the same placement:
+ * MOE_A2A_P2P latches MOE_ERR_DEVICE on the device (reported by the next
+ * synchronising call); MOE_A2A_NCCL returns MOE_ERR_DEVICE from this call.
  * CUDA graphs: a whole layer (moe_route .. moe_combine) may be captured and
  * replayed on a stream (not in MOE_A2A_NCCL mode, whose dispatch reads the
  * counts on the host).  In MOE_A2A_P2P mode the flag epoch lives on the device

@@ -45,6 +45,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
+// Per-device "done once" bit (function attributes are set per device; a process may
+// drive several devices).  Returns true the first time for the current device.
+inline bool first_time_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
+}
+
 // ---------------------------------------------------------------- bulk async copies (TMA engine, no tensor map)
 // shared::cta -> global (local or NVLink peer memory), completion tracked per thread in bulk groups
 __device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t ssrc, uint32_t bytes) {

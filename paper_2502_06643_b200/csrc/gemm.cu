@@ -573,11 +573,10 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
                                const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride) {
   using C = GemmCfg<BN, CG, FUSED>;
   auto kern = k_grouped_gemm<BN, SWIGLU, CG, FUSED>;
-  static bool configured = false;
-  if (!configured) {
+  static unsigned long long configured = 0;  // per device
+  if (first_time_on_device(configured)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(tmA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(tmB);

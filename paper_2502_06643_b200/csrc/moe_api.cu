@@ -46,6 +46,8 @@ struct moe_ctx {
   int32_t* row_of_item = nullptr;
   int* err_dev = nullptr;
   int32_t* cnt_pinned = nullptr;  // host copy of cnt_all (NCCL mode / debug)
+  uint32_t* phash_dev = nullptr;  // NCCL mode: [G] all-gathered placement hashes + [1] this rank's
+  uint32_t* phash_pinned = nullptr;  // [G + 1] host staging
 
   // payload buffers
   int64_t cap_rows = 0;      // receive-layout rows (padded)
@@ -428,7 +430,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   cudaMemset(ctx->epoch_dev, 0, sizeof(unsigned));
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess) {
+      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->phash_pinned, sizeof(uint32_t) * (size_t)(G + 1)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->phash_dev, sizeof(uint32_t) * (size_t)(G + 1)) != cudaSuccess) {
     fail(ctx, MOE_ERR_CUDA, "cudaMallocHost failed");
     return bail(MOE_ERR_CUDA);
   }
@@ -567,6 +571,8 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->P_pinned) cudaFreeHost(ctx->P_pinned);
   if (ctx->cnt_pinned) cudaFreeHost(ctx->cnt_pinned);
+  if (ctx->phash_pinned) cudaFreeHost(ctx->phash_pinned);
+  if (ctx->phash_dev) cudaFree(ctx->phash_dev);
   delete ctx;
   return MOE_OK;
 }
@@ -715,10 +721,24 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   LAUNCHED(ctx, (a.n_tiles > 0) + 1);
   const bool nccl = ctx->comm != nullptr && !ctx->p2p;
   if (nccl) {
+    // the counts and a hash of the placement: all ranks must dispatch with the same map
+    uint32_t h = 2166136261u;
+    for (int e = 0; e < E; ++e) h = (h ^ (uint32_t)expert_to_rank[e]) * 16777619u;
+    ctx->phash_pinned[G] = h;
+    CU(cudaMemcpyAsync(ctx->phash_dev + G, ctx->phash_pinned + G, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    NC(ncclGroupStart());
     NC(ncclAllGather(ctx->cnt_local, ctx->cnt_all, E, ncclInt32, ctx->comm, s));
+    NC(ncclAllGather(ctx->phash_dev + G, ctx->phash_dev, 1, ncclUint32, ctx->comm, s));
+    NC(ncclGroupEnd());
     CU(cudaMemcpyAsync(ctx->cnt_pinned, ctx->cnt_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ctx->phash_pinned, ctx->phash_dev, sizeof(uint32_t) * G, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     memcpy(ctx->cnt_host.data(), ctx->cnt_pinned, sizeof(int32_t) * G * E);
+    for (int g = 0; g < G; ++g)
+      if (ctx->phash_pinned[g] != h) {
+        ctx->have_plan = false;
+        return fail(ctx, MOE_ERR_DEVICE, "ranks dispatched with different expert_to_rank maps (rank %d differs)", g);
+      }
   }
   launch_layout(a, b, ctx->cap_rows, s);  // P2P: also the in-kernel count all-gather
   tl_rec(ctx, 1, s);

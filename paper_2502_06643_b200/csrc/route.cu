@@ -155,11 +155,9 @@ void launch_route_stats(const int32_t* idx_l, const int32_t* idx_l1, int T, int 
   if (blocks > 2 * num_sms) blocks = 2 * num_sms;
   const int smem_co = E <= 128 ? 1 : 0;
   size_t smem = sizeof(int) * (E + (idx_l1 && smem_co ? E * E : 0));
-  static bool attr = false;
-  if (!attr) {  // E up to 128 needs > 48 KB for the E x E histogram
+  static unsigned long long attr = 0;  // per device
+  if (first_time_on_device(attr))  // E up to 128 needs > 48 KB for the E x E histogram
     cudaFuncSetAttribute(k_route_stats, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(int) * (128 + 128 * 128)));
-    attr = true;
-  }
   k_route_stats<<<blocks, threads, smem, s>>>(idx_l, idx_l1, T, E, k, (unsigned long long*)load,
                                               (unsigned long long*)coact, err, smem_co);
 }

@@ -184,18 +184,18 @@ def main():
         if b2 > a2:
             assert torch.equal(out.view(torch.int16), virt_out[a2:b2].view(torch.int16)), "small-T equality"
     # call discipline: ranks passing different placements to one dispatch are caught
-    # on the device (P2P: the placement hash travels with the counts)
-    if lay.a2a == "p2p":
-        bad = np.array([e * world // E for e in range(E)])
-        if rank == world - 1:
-            bad = bad[::-1].copy()
-        idx, w = lay.route(ls, k) if b2 > a2 else lay.route(logits[:0], k)
+    # (P2P: the placement hash travels with the counts and is checked on the device;
+    # NCCL: it is all-gathered with the counts and checked on the host)
+    bad = np.array([e * world // E for e in range(E)])
+    if rank == world - 1:
+        bad = bad[::-1].copy()
+    idx, w = lay.route(ls, k) if b2 > a2 else lay.route(logits[:0], k)
+    try:
         lay.dispatch(xs if b2 > a2 else x[:0], idx, bad)
-        try:
-            lay.sync()
-            raise AssertionError("placement mismatch not detected")
-        except moe.MoeError as ex:
-            assert "different expert_to_rank" in str(ex), str(ex)
+        lay.sync()
+        raise AssertionError("placement mismatch not detected")
+    except moe.MoeError as ex:
+        assert "different expert_to_rank" in str(ex), str(ex)
     lay.close()
     dist.barrier()
     dist.destroy_process_group()
