@@ -125,7 +125,8 @@ int32_t moe_abi_version(void);                            /* MOE_ABI_VERSION */
  * For each token t: idx[t][0..k-1] = the k largest logits[t][.] in descending
  * order, ties to the lower expert id, -0.0 == +0.0; w[t][j] = softmax over the
  * k selected logits = exp(l_j - l_0) / sum_j' exp(l_j' - l_0) (fp32).
- * logits: float [T][E]; idx: int32 [T][k]; w: float [T][k].  Rank-local. */
+ * logits: float [T][E]; idx: int32 [T][k]; w: float [T][k].  Rank-local.
+ * A NaN logit latches MOE_ERR_DEVICE (reading G3: logits are finite). */
 moe_status moe_route(moe_ctx_t ctx, const float* logits, int32_t T, int32_t E, int32_t k,
                      int32_t* idx, float* w, moe_stream_t stream);
 

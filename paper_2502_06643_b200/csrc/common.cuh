@@ -24,6 +24,7 @@ constexpr int kErrBadExpert = 1;
 constexpr int kErrCapacity = 2;
 constexpr int kErrTimeout = 4;  // a P2P peer flag never arrived
 constexpr int kErrPlacement = 8;  // ranks passed different expert_to_rank maps to one dispatch
+constexpr int kErrNaN = 16;       // a router logit is NaN (reading G3: logits are finite)
 constexpr unsigned long long kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -6,7 +6,7 @@
 namespace moe {
 
 // K1 / K9 (route.cu)
-void launch_route(const float* logits, int T, int E, int k, int32_t* idx, float* w, cudaStream_t s);
+void launch_route(const float* logits, int T, int E, int k, int32_t* idx, float* w, int* err, cudaStream_t s);
 void launch_route_stats(const int32_t* idx_l, const int32_t* idx_l1, int T, int E, int k, int64_t* load,
                         int64_t* coact, int* err, int num_sms, cudaStream_t s);
 

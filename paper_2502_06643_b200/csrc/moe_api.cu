@@ -582,11 +582,12 @@ static moe_status check_device_error(moe_ctx_t ctx) {
   CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   if (e) {
     cudaMemset(ctx->err_dev, 0, sizeof(int));
-    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s",
+    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s%s",
                 (e & kErrBadExpert) ? " expert id out of range" : "",
                 (e & kErrCapacity) ? " receive capacity exceeded" : "",
                 (e & kErrTimeout) ? " P2P peer flag timeout (a rank skipped a collective call?)" : "",
-                (e & kErrPlacement) ? " ranks dispatched with different expert_to_rank maps" : "");
+                (e & kErrPlacement) ? " ranks dispatched with different expert_to_rank maps" : "",
+                (e & kErrNaN) ? " NaN router logit" : "");
   }
   return MOE_OK;
 }
@@ -608,7 +609,7 @@ moe_status moe_route(moe_ctx_t ctx, const float* logits, int32_t T, int32_t E, i
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   if (T == 0) return MOE_OK;
-  launch_route(logits, T, E, k, idx, w, s);
+  launch_route(logits, T, E, k, idx, w, ctx->err_dev, s);
   LAUNCHED(ctx, 1);
   return MOE_OK;
 }

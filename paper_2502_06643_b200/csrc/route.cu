@@ -26,7 +26,7 @@ __device__ __forceinline__ float key_to_float(uint32_t k) {
 // winner of a round is the largest remaining logit, ties to the lower id.
 template <int LPT, int VPL>
 __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits, int T, int E, int k,
-                                               int32_t* __restrict__ idx, float* __restrict__ w) {
+                                               int32_t* __restrict__ idx, float* __restrict__ w, int* err) {
   constexpr int TPW = 32 / LPT;  // tokens per warp
   const int lane = threadIdx.x & 31;
   const int gl = lane % LPT;
@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
     const int e = gl + v * LPT;
     if (valid && e < E) {
       float l = __ldg(logits + t * E + e) + 0.0f;  // -0.0 -> +0.0
+      if (l != l) atomicOr(err, kErrNaN);           // NaN: the selection is undefined
       key[v] = ((uint64_t)ordered_key(l) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)e);
     } else {
       key[v] = 0;  // below every real key
@@ -75,13 +76,13 @@ __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits,
   }
 }
 
-void launch_route(const float* logits, int T, int E, int k, int32_t* idx, float* w, cudaStream_t s) {
+void launch_route(const float* logits, int T, int E, int k, int32_t* idx, float* w, int* err, cudaStream_t s) {
   if (T <= 0) return;
   const int threads = 256;
   auto go = [&](auto kern, int lpt) {
     long long tokens_per_block = (threads / 32) * (32 / lpt);
     int blocks = (int)((T + tokens_per_block - 1) / tokens_per_block);
-    kern<<<blocks, threads, 0, s>>>(logits, T, E, k, idx, w);
+    kern<<<blocks, threads, 0, s>>>(logits, T, E, k, idx, w, err);
   };
   if (E <= 4) go(k_route<4, 1>, 4);
   else if (E <= 8) go(k_route<8, 1>, 8);

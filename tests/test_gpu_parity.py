@@ -60,6 +60,20 @@ def test_route_empty(cuda_ok):
     assert idx.shape == (0, 2)
 
 
+def test_route_nan_logit_latches_device_error(cuda_ok):
+    """Reading G3: router logits are finite; a NaN latches MOE_ERR_DEVICE."""
+    moe = _moe()
+    lay = make_layer(64, 64, 64, 8, 2)
+    logits = torch.randn(64, 8, device=DEV)
+    logits[5, 3] = float("nan")
+    lay.route(logits, 2)
+    with pytest.raises(moe.MoeError) as ei:
+        lay.sync()
+    assert ei.value.status == 6 and "NaN" in str(ei.value)
+    lay.route(torch.randn(64, 8, device=DEV), 2)     # the error word was cleared
+    lay.sync()
+
+
 # ------------------------------------------------------------------ a2
 @pytest.mark.parametrize("T,E,k", [(5000, 8, 2), (1031, 64, 8), (333, 128, 4), (1, 8, 2), (777, 256, 16), (300, 200, 3)])
 def test_route_stats_bit_exact(cuda_ok, T, E, k):
