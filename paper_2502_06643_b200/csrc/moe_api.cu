@@ -843,11 +843,11 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const int nw = ctx->n_hosted;
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
-  // Fused combine (K6 returns rows over NVLink, row-coalesced through smem): pays off
-  // when the combine's NVLink time is a sizeable fraction of K6's tensor time, i.e.
-  // t_nvl/t_gemm ~ 1.8e3 / F -- measured -7% per layer at F = 2048 (E64, 4EP) and
-  // +1.5% at F = 14336 (Mixtral, 4EP; K6 loses two pipeline stages to the staging
-  // buffer), profiles/r1_v8_*.  Default: on for F <= 8192; MOE_FUSED_COMBINE=0/1 overrides.
+  // Fused combine (K6 returns rows over NVLink, staged in smem, one bulk copy per
+  // row piece): pays off when the combine's NVLink time is a sizeable fraction of
+  // K6's tensor time, t_nvl/t_gemm ~ 1.8e3 / F -- measured -7% per layer at F = 2048
+  // (E64, 4EP; profiles/r1_v8_*) and no difference at F = 14336 (Mixtral 2/4EP,
+  // gpurun call 47).  Default: on for F/tp <= 8192; MOE_FUSED_COMBINE=0/1 overrides.
   {
     bool fused = ctx->Fl <= 8192;
     if (const char* env = getenv("MOE_FUSED_COMBINE")) fused = atoi(env) != 0;
