@@ -217,7 +217,10 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   // K3/K8 CTAs (512 threads) fit twice per SM, so aim at <= 2 x num_sms CTAs
   const int chunks = c->H / 8;
   int split = a.n_tiles > 0 ? (2 * c->num_sms) / a.n_tiles : 1;
-  split = std::max(1, std::min(split, std::min(8, chunks / 32 > 0 ? chunks / 32 : 1)));
+  // (at most 32 slices of >= 16 16-byte chunks each: decode-sized batches have one
+  // or two token tiles, and every slice is another CTA pulling/pushing rows)
+  static const int cap = getenv("MOE_COL_SPLIT_MAX") ? std::max(1, atoi(getenv("MOE_COL_SPLIT_MAX"))) : 32;
+  split = std::max(1, std::min(split, std::min(cap, chunks / 16 > 0 ? chunks / 16 : 1)));
   a.col_split = split;
   return a;
 }
