@@ -49,8 +49,13 @@ struct GemmCfg {
   // row pitch padded by 16 bytes so the lane-per-row writes are conflict-free);
   // each row then leaves as one bulk async copy (TMA engine) to its destination
   static constexpr int STAGE_PITCH = BN * 2 + 16;
-  static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 0;
-  static constexpr int BUDGET = kSmemBudget - STAGING;
+  // plain / SwiGLU epilogues: each warp stages a 32-row x 32-column bf16 chunk
+  // (pitch 80 B: conflict-free lane-per-row writes) and writes it back with
+  // row-contiguous 64-byte segments (full 32-byte sectors) instead of one
+  // 16-byte piece of 32 different rows per store instruction
+  static constexpr int EPI_PITCH = 80;
+  static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 4 * 32 * EPI_PITCH;
+  static constexpr int BUDGET = (FUSED ? kSmemBudget : kSmemBudget + 10 * 1024) - STAGING;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
@@ -115,6 +120,25 @@ __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile
   wrow = sg.wrow[i];
 }
 
+// One warp's 32 rows x 32 bf16 columns (lane = row, packed = its 64 bytes) ->
+// D[wrow0 + r][col0 .. col0 + 32): staged in smem (pitch 80 B, conflict-free),
+// then written as 64-byte row segments, 8 rows per store instruction.
+__device__ __forceinline__ void epi_store_chunk(uint8_t* stg, const uint32_t (&packed)[16], uint16_t* D, int ldd,
+                                                long long wrow0, long long col0, int lane) {
+  uint4* mine = reinterpret_cast<uint4*>(stg + lane * 80);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mine[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int idx = j * 32 + lane;        // (row, 16-byte piece) = (idx / 4, idx % 4)
+    const int r = idx >> 2, piece = idx & 3;
+    const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 80 + piece * 16);
+    *reinterpret_cast<uint4*>(D + (wrow0 + r) * ldd + col0 + piece * 8) = v;
+  }
+  __syncwarp();
+}
+
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -130,7 +154,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   static_assert(sizeof(SegSmem) <= 8192, "segment table");
   SegSmem& sg = *reinterpret_cast<SegSmem*>(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES + 8192);
-  uint8_t* staging = smem + C::STAGES * C::STAGE_BYTES + 8192 + 512;  // FUSED: 4 warps x 32 rows x BN bf16
+  uint8_t* staging = smem + C::STAGES * C::STAGE_BYTES + 8192 + 512;  // per epilogue warp (see GemmCfg)
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -424,7 +448,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                  __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
         }
       } else if constexpr (SWIGLU) {
-        uint16_t* drow = D + grow * ldd + (long long)nt * (BN / 2);
+        uint8_t* stg = staging + (size_t)(warp - 2) * 32 * C::EPI_PITCH;
+        const long long wrow0 = arow + (int)crank * 128 + q * 32;  // first row of this warp
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
           uint32_t g[32], u[32];
@@ -440,10 +465,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const float h1 = g1 / (1.0f + __expf(-g1)) * u1;
             packed[i] = pack_bf16x2(h0, h1);
           }
-          uint4* dst = reinterpret_cast<uint4*>(drow + c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * (BN / 2) + c, lane);
         }
       } else if constexpr (FUSED) {
         // Fused combine: the row belongs to source s (rows of s are contiguous in the
@@ -493,7 +515,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           bulk_commit();
         }
       } else {
-        uint16_t* drow = D + grow * ldd + (long long)nt * BN;
+        uint8_t* stg = staging + (size_t)(warp - 2) * 32 * C::EPI_PITCH;
+        const long long wrow0 = arow + (int)crank * 128 + q * 32;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t v[32];
@@ -502,10 +525,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          uint4* dst = reinterpret_cast<uint4*>(drow + c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * BN + c, lane);
         }
       }
       if (FUSED && ksplit > 1) {  // (never launched: split-K is not combined with the fused combine)
