@@ -125,6 +125,12 @@ __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile
 // then written as 64-byte row segments, 8 rows per store instruction.
 __device__ __forceinline__ void epi_store_chunk(uint8_t* stg, const uint32_t (&packed)[16], uint16_t* D, int ldd,
                                                 long long wrow0, long long col0, int lane) {
+#ifdef MOE_EPI_DIRECT  // A/B builds: the lane writes its own row's 64 bytes directly
+  uint4* dst = reinterpret_cast<uint4*>(D + (wrow0 + lane) * ldd + col0);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  return;
+#endif
   uint4* mine = reinterpret_cast<uint4*>(stg + lane * 80);
 #pragma unroll
   for (int i = 0; i < 4; ++i) mine[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
