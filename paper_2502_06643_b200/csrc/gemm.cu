@@ -523,27 +523,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       } else {
         uint8_t* stg = staging + (size_t)(warp - 2) * 32 * C::EPI_PITCH;
         const long long wrow0 = arow + (int)crank * 128 + q * 32;
-#ifndef MOE_EPI_ONE_LD
-        constexpr int CH = BN >= 64 ? 64 : 32;  // columns per TMEM round trip (two loads in flight)
-#else
-        constexpr int CH = 32;
-#endif
 #pragma unroll 1
-        for (int c = 0; c < BN; c += CH) {
-          uint32_t v0[32], v1[32];
-          tmem_ld32(taddr + c, v0);
-          if constexpr (CH == 64) tmem_ld32(taddr + c + 32, v1);
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c, v);
           tmem_ld_wait();
           uint32_t packed[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v0[2 * i]), __uint_as_float(v0[2 * i + 1]));
+          for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
           epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * BN + c, lane);
-          if constexpr (CH == 64) {
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              packed[i] = pack_bf16x2(__uint_as_float(v1[2 * i]), __uint_as_float(v1[2 * i + 1]));
-            epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * BN + c + 32, lane);
-          }
         }
       }
       if (FUSED && ksplit > 1) {  // (never launched: split-K is not combined with the fused combine)
