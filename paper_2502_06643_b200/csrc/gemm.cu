@@ -49,11 +49,14 @@ struct GemmCfg {
   // row pitch padded by 16 bytes so the lane-per-row writes are conflict-free);
   // each row then leaves as one bulk async copy (TMA engine) to its destination
   static constexpr int STAGE_PITCH = BN * 2 + 16;
-  // plain / SwiGLU epilogues: each warp stages a 32-row x 32-column bf16 chunk
-  // (pitch 80 B: conflict-free lane-per-row writes) and writes it back with
-  // row-contiguous 64-byte segments (full 32-byte sectors) instead of one
-  // 16-byte piece of 32 different rows per store instruction
+  // plain / SwiGLU epilogues: each warp stages 32-row x 32-column bf16 chunks in
+  // a 2 KB buffer (dense 64-byte rows) and one lane stores each chunk with a
+  // TMA 2D store (async: the warp moves on to the next TMEM chunk while the
+  // copy engine writes the rows).  Measured: the output stores were costing the
+  // GEMMs ~10% (profiles/r1_v17_*).  MOE_EPI_LSU builds the LSU variant instead
+  // (pitch 80 B, 64-byte row segments stored by all lanes).
   static constexpr int EPI_PITCH = 80;
+  static constexpr int EPI_BUF = 32 * 64;
   static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 4 * 32 * EPI_PITCH;
   static constexpr int BUDGET = (FUSED ? kSmemBudget : kSmemBudget + 10 * 1024) - STAGING;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
@@ -123,8 +126,33 @@ __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile
 // One warp's 32 rows x 32 bf16 columns (lane = row, packed = its 64 bytes) ->
 // D[wrow0 + r][col0 .. col0 + 32): staged in smem (pitch 80 B, conflict-free),
 // then written as 64-byte row segments, 8 rows per store instruction.
+// TMA variant: the chunk goes to the warp's 2 KB staging buffer; lane 0 issues the
+// store after every lane wrote its row and fenced it for the async proxy.  (One
+// buffer per warp: two would push K5 past the shared memory that lets a k_scatter
+// CTA co-reside with it in P2P mode.)
+__device__ __forceinline__ void epi_store_chunk_tma(uint8_t* stg, int n, const uint32_t (&packed)[16],
+                                                    const CUtensorMap* tmD, int wrow0, int col0, int lane) {
+  (void)n;
+  uint8_t* buf = stg;
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous chunk was read
+  __syncwarp();
+  uint4* mine = reinterpret_cast<uint4*>(buf + lane * 64);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) mine[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(tmD, buf, col0, wrow0);
+    bulk_commit();
+  }
+}
+
 __device__ __forceinline__ void epi_store_chunk(uint8_t* stg, const uint32_t (&packed)[16], uint16_t* D, int ldd,
                                                 long long wrow0, long long col0, int lane) {
+#ifdef MOE_EPI_NOSTORE  // timing experiment only (wrong results): no output stores
+  if (lane < 0) D[0] = (uint16_t)packed[0];
+  return;
+#endif
 #ifdef MOE_EPI_DIRECT  // A/B builds: the lane writes its own row's 64 bytes directly
   uint4* dst = reinterpret_cast<uint4*>(D + (wrow0 + lane) * ldd + col0);
 #pragma unroll
@@ -150,7 +178,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
                    int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf,
-                   int tile_ahead, int ksplit, float* __restrict__ part, long long part_stride) {
+                   int tile_ahead, int ksplit, float* __restrict__ part, long long part_stride,
+                   const __grid_constant__ CUtensorMap tmD) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   extern __shared__ uint8_t smem_raw[];
@@ -471,7 +500,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const float h1 = g1 / (1.0f + __expf(-g1)) * u1;
             packed[i] = pack_bf16x2(h0, h1);
           }
+#ifndef MOE_EPI_LSU
+          epi_store_chunk_tma(stg, c / 32, packed, &tmD, (int)wrow0, nt * (BN / 2) + c, lane);
+#else
           epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * (BN / 2) + c, lane);
+#endif
         }
       } else if constexpr (FUSED) {
         // Fused combine: the row belongs to source s (rows of s are contiguous in the
@@ -531,7 +564,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+#ifndef MOE_EPI_LSU
+          epi_store_chunk_tma(stg, c / 32, packed, &tmD, (int)wrow0, nt * BN + c, lane);
+#else
           epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * BN + c, lane);
+#endif
         }
       }
       if (FUSED && ksplit > 1) {  // (never launched: split-K is not combined with the fused combine)
@@ -559,6 +596,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       bulk_wait_all();
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence_system();
+    } else {                // the epilogue's TMA stores have landed before the kernel ends
+      if (lane == 0) bulk_wait_all();
+      __syncwarp();
     }
   }
 
@@ -596,7 +636,8 @@ int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu)
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
                                int N, int K, int num_sms, const SrcWait& sw, int* err, unsigned* sched,
-                               const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride) {
+                               const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride,
+                               const void* tmD) {
   using C = GemmCfg<BN, CG, FUSED>;
   auto kern = k_grouped_gemm<BN, SWIGLU, CG, FUSED>;
   static unsigned long long configured = 0;  // per device
@@ -606,6 +647,9 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   }
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(tmA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(tmB);
+  // output map of the TMA-store epilogue (any valid map when the epilogue does not
+  // use it: fused combine, split-K partials)
+  const CUtensorMap& dmap = *reinterpret_cast<const CUtensorMap*>(tmD ? tmD : tmA);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((num_sms / CG) * CG);
   cfg.blockDim = dim3(kGemmThreads);
@@ -647,19 +691,19 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
     ahead = (env && atoi(env) != 0) ? 1 : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
-                            sched, fr, pf, ahead, ksplit, part, part_stride);
+                            sched, fr, pf, ahead, ksplit, part, part_stride, dmap);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
                                 unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit, float* part,
-                                long long part_stride) {
+                                long long part_stride, const void* tmD) {
   const int bn = gemm_block_n(N, swiglu);
   if (ksplit < 1) ksplit = 1;
   const bool fused = fr.enabled && !swiglu;
 #define MOE_GO(BN_, SW_, CG_, FU_) \
   launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s, ksplit, part, \
-                                  part_stride)
+                                  part_stride, tmD)
 #define MOE_GO2(BN_, CG_) (fused ? MOE_GO(BN_, false, CG_, true) : MOE_GO(BN_, false, CG_, false))
   if (cg == 2) {
     if (swiglu) return bn == 256 ? MOE_GO(256, true, 2, false) : MOE_GO(128, true, 2, false);
@@ -770,6 +814,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
   return make_tmap_2d_ld(tmap_out, base, rows, cols, cols, box_rows);
+}
+
+bool make_tmap_store_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {32, 32};  // one epilogue chunk: 32 rows x 32 bf16 (dense 64-byte rows)
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 bool make_tmap_2d_ld(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,

@@ -129,7 +129,8 @@ int pack_block(int F);
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
                                 int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
                                 unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit = 1,
-                                float* part = nullptr, long long part_stride = 0);
+                                float* part = nullptr, long long part_stride = 0, const void* tmD = nullptr);
+// tmD: TMA-store map of D (make_tmap_store_2d) for the plain / SwiGLU epilogues.
 // ksplit > 1 (plain GEMMs, no fused combine): fp32 partials of the K slices go to
 // part[slice][row][N]; launch_splitk_reduce then writes D = bf16(sum over slices).
 cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
@@ -144,5 +145,7 @@ bool make_tmap_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols
 // Same with a row pitch of ld elements (a column slice of a wider matrix).
 bool make_tmap_2d_ld(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                      uint32_t box_rows);
+// Store map for the GEMM epilogue: bf16 [rows][cols] with pitch ld, box {32, 32}, no swizzle.
+bool make_tmap_store_2d(void* tmap_out, const void* base, uint64_t rows, uint64_t cols, uint64_t ld);
 
 }  // namespace moe

@@ -62,6 +62,9 @@ struct moe_ctx {
   alignas(64) uint8_t tmB1[128];
   alignas(64) uint8_t tmB2[128];
   alignas(64) uint8_t tmA2s[kMaxTP][128];  // virtual TP: h column slice q
+  alignas(64) uint8_t tmDh[128];           // epilogue TMA-store maps: h [cap][Fl]
+  alignas(64) uint8_t tmDy[128];           //   y [cap][H]
+  alignas(64) uint8_t tmDys[kMaxTP][128];  //   virtual TP: partial-output buffer q
   alignas(64) uint8_t tmB2s[kMaxTP][128];  // virtual TP: W2 column slice q
   const void* tmB1_ptr = nullptr;
   const void* tmB2_ptr = nullptr;
@@ -447,6 +450,18 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
     return bail(MOE_ERR_CUDA);
   }
+  if (!make_tmap_store_2d(ctx->tmDh, ctx->hbuf, ctx->cap_rows, ctx->Fl, ctx->Fl) ||
+      !make_tmap_store_2d(ctx->tmDy, ctx->ybuf, ctx->cap_rows, c.hidden, c.hidden)) {
+    fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the epilogue store maps");
+    return bail(MOE_ERR_CUDA);
+  }
+  if (ctx->virt && tp > 1)
+    for (int q = 0; q < tp; ++q)
+      if (!make_tmap_store_2d(ctx->tmDys[q], ctx->ybuf + (size_t)q * ctx->cap_rows * c.hidden, ctx->cap_rows,
+                              c.hidden, c.hidden)) {
+        fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for a partial-output store map");
+        return bail(MOE_ERR_CUDA);
+      }
   if (ctx->virt && tp > 1)
     for (int q = 0; q < tp; ++q)
       if (!make_tmap_2d_ld(ctx->tmA2s[q], ctx->hbuf + (size_t)q * (c.ffn / tp), ctx->cap_rows, c.ffn / tp, c.ffn,
@@ -934,7 +949,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   const long long pstride5 = (long long)ctx->cap_rows * 2 * F;
   cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
                                       ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
-                                      s, ksplit5, ctx->splitk_ws, pstride5);
+                                      s, ksplit5, ctx->splitk_ws, pstride5, ctx->tmDh);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
   if (ksplit5 > 1) {
     e = launch_splitk_reduce_swiglu(ctx->splitk_ws, pstride5, ksplit5, ctx->seg_meta, ctx->E, F, ctx->gemm_cg,
@@ -948,7 +963,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     const long long pstride = (long long)ctx->cap_rows * H;
     e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
                             ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s, ksplit,
-                            ctx->splitk_ws, pstride);
+                            ctx->splitk_ws, pstride, ctx->tmDy);
     if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
     if (ksplit > 1) {
       e = launch_splitk_reduce(ctx->splitk_ws, pstride, ksplit, ctx->seg_meta, ctx->E, H, ctx->gemm_cg, ctx->ybuf, H,
@@ -962,7 +977,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     for (int q = 0; q < tp; ++q) {
       e = launch_grouped_gemm(ctx->tmA2s[q], ctx->tmB2s[q], ctx->ybuf + (size_t)q * ctx->cap_rows * H, H,
                               ctx->seg_meta, ctx->E, H, F / tp, false, ctx->gemm_cg, ctx->num_sms, nowait,
-                              ctx->err_dev, ctx->done_counter + 2, plain, s);
+                              ctx->err_dev, ctx->done_counter + 2, plain, s, 1, nullptr, 0, ctx->tmDys[q]);
       if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 slice launch: %s", cudaGetErrorString(e));
     }
     ctx->launches += tp - 1;
