@@ -142,7 +142,11 @@ __device__ __forceinline__ void epi_store_chunk_tma(uint8_t* stg, int n, const u
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
+#ifndef MOE_EPI_NO_EVICT_FIRST
+    tma_store_2d_hint(tmD, buf, col0, wrow0, l2_evict_first_policy());
+#else
     tma_store_2d(tmD, buf, col0, wrow0);
+#endif
     bulk_commit();
   }
 }
