@@ -394,13 +394,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (CG == 2) {
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-#ifdef MOE_LOAD_HINTS  // (experiment) A group resident (evict_last), weights streamed (evict_first)
-            tma_load_2d_pair_hint(&tmA, fb, smA + stage * C::A_BYTES, kb * BK, a_row, l2_evict_last_policy());
-            tma_load_2d_pair_hint(&tmB, fb, smB + stage * C::B_BYTES, kb * BK, b_row, l2_evict_first_policy());
-#else
             tma_load_2d_pair(&tmA, fb, smA + stage * C::A_BYTES, kb * BK, a_row);
             tma_load_2d_pair(&tmB, fb, smB + stage * C::B_BYTES, kb * BK, b_row);
-#endif
           } else {
             mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
             tma_load_2d(&tmA, &full[stage], smA + stage * C::A_BYTES, kb * BK, a_row);
