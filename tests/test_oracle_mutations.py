@@ -72,6 +72,22 @@ def test_receive_order_source_major_is_caught(monkeypatch):
     _fails(t_plan.test_receive_order_brute_force)
 
 
+def test_send_order_by_expert_only_is_caught(monkeypatch):
+    orig = plan.plan
+
+    def bad(idx_by_source, P, G):           # send order keyed by e alone, not (P[e], e) (not G9)
+        pl = orig(idx_by_source, P, G)
+        for s, idx in enumerate(idx_by_source):
+            idx = np.asarray(idx)
+            order = np.argsort(idx.ravel(), kind="stable")
+            sl = np.empty(len(order), dtype=np.int64)
+            sl[order] = np.arange(len(order))
+            pl["slot"][s] = sl.reshape(idx.shape)
+        return pl
+    monkeypatch.setattr(plan, "plan", bad)
+    _fails(t_plan.test_send_order_groups_by_destination, 4, [0, 1, 2, 2, 3, 2, 3, 3])
+
+
 def test_unpermute_without_gate_weights_is_caught(monkeypatch):
     def bad(ret_rows, w):                   # sums the k expert rows, drops the gate weights
         acc = np.zeros_like(ret_rows[0])

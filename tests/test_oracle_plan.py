@@ -78,6 +78,36 @@ def test_receive_order_brute_force():
         assert [(s, t, j, e) for (e, s, t, j) in items] == pl["recv"][g]
 
 
+@pytest.mark.parametrize("G,P", [(4, [0, 1, 2, 2, 3, 2, 3, 3]),       # ILP-1 balanced, non-monotone
+                                 (3, [2, 2, 2, 0, 0, 0, 0, 0]),       # destinations in descending expert order
+                                 (3, [1, 0, 2, 1, 1, 0, 2]),          # E = 7, interleaved
+                                 (4, [3, 3, 3, 3, 3, 3, 1, 1])])      # ranks hosting no expert (G13)
+def test_send_order_groups_by_destination(G, P):
+    """G9 send order (tokens are sent to the GPU hosting their assigned
+    expert): a source's send buffer is one contiguous run per destination rank, the
+    runs in rank order, so the run for rank g starts at sum_{g' < g} send_counts[s][g']
+    and has send_counts[s][g] items; inside a run the items are ordered by
+    (expert, token, slot j).  Non-monotone placements make this differ from a plain
+    sort by expert id."""
+    rng = np.random.default_rng(len(P) * 10 + G)
+    E, k = len(P), 3
+    T_s = [40, 17, 29, 0][:G]
+    idxs = [_idx(rng, n, E, k) for n in T_s]
+    pl = plan.plan(idxs, P, G)
+    for s in range(G):
+        idx = idxs[s]
+        start = 0
+        for g in range(G):
+            n = int(pl["send_counts"][s][g])
+            items = [(int(idx[t, j]), t, j) for t in range(idx.shape[0]) for j in range(k) if P[idx[t, j]] == g]
+            assert len(items) == n
+            slots = sorted(int(pl["slot"][s][t, j]) for (_, t, j) in items)
+            assert slots == list(range(start, start + n))           # contiguous run, in rank order
+            by_slot = sorted(items, key=lambda it: pl["slot"][s][it[1], it[2]])
+            assert by_slot == sorted(items)                          # (e, t, j) order inside the run
+            start += n
+
+
 def test_token_blocks():
     assert plan.token_blocks(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
     assert plan.token_blocks(3, 4) == [(0, 1), (1, 2), (2, 3), (3, 3)]
