@@ -400,48 +400,80 @@ def run_ours(args):
                                "measured peer copy (B200_PROFILING.md)"},
             k5_ms=float(np.mean(k5)) if k5 else None, k6_ms=float(np.mean(k6)) if k6 else None,
             rows_rank0=rows_here)
-        # per-phase breakdown (separate, untimed-for-value loop): the paper's
-        # "token processing time" (expert FFN) and "all-to-all time" (dispatch +
-        # combine), tail = max over GPUs and average = mean over GPUs
+        # Per-phase breakdown: a separate loop (not part of `value`) that runs the
+        # layer with each phase SERIALISED -- a device sync and a barrier between
+        # dispatch, expert FFN and combine -- so every window holds only this rank's
+        # own work: the expert-FFN window is pure token processing (no waiting for
+        # peers' rows), the dispatch / combine windows are the all-to-alls (the
+        # dispatch's side-stream push of the peers' rows included, via the library's
+        # timeline events).  The paper's metrics: tail = max over GPUs,
+        # average = mean over GPUs, of "token processing" (expert FFN) and
+        # "all-to-all" (dispatch + combine) time.
         nph = 5
-        phase = np.zeros((nph, 5))
+        phase = np.zeros((nph, 7))
+        lay.timeline(nph)
         for i in range(nph):
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
             barrier()
+            torch.cuda.synchronize()
             evs[0].record(stream)
             lay.route(logits, k, idx, wts)
-            evs[1].record(stream)
             lay.route_stats(idx_prev, idx, load, coact)
-            evs[2].record(stream)
+            evs[1].record(stream)
             lay.dispatch(x, idx, P)
-            evs[3].record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            evs[2].record(stream)
             lay.expert_ffn(w13, w2)
+            evs[3].record(stream)
+            torch.cuda.synchronize()
+            barrier()
             evs[4].record(stream)
             lay.combine(wts, out)
             evs[5].record(stream)
             torch.cuda.synchronize()
-            phase[i] = [evs[j].elapsed_time(evs[j + 1]) for j in range(5)]
-        pm = phase.mean(0)
+            phase[i, :3] = [evs[0].elapsed_time(evs[1]), evs[2].elapsed_time(evs[3]), evs[4].elapsed_time(evs[5])]
+        tl = np.array(lay.timeline_read())         # [nph][8] ms after dispatch entry (moe.h)
+        lay.timeline(0)
+        # dispatch window: entry -> both scatters done (own rows on the stream, peers'
+        # rows on the side stream); peers'-rows push window: layout done -> side scatter done
+        phase[:, 3] = np.maximum(tl[:, 2], tl[:, 3])
+        phase[:, 4] = np.maximum(tl[:, 3] - tl[:, 1], 1e-6)
+        phase[:, 5] = tl[:, 5] - tl[:, 4]          # K5 (serialised: no arrival waits)
+        phase[:, 6] = tl[:, 6] - tl[:, 5]          # K6 (fused combine: includes the NVLink returns)
+        pm = np.median(phase, 0)
+        names = ["route_and_stats", "expert_ffn", "combine", "dispatch", "dispatch_push", "k5", "k6"]
         tail = max_over_ranks(list(pm))
         avg = mean_over_ranks(list(pm))
-        names = ["route", "route_stats", "dispatch", "expert_ffn", "combine"]
-        res["phases_ms"] = {"tail": dict(zip(names, map(float, tail))), "avg": dict(zip(names, map(float, avg)))}
+        res["phases_ms_serialised"] = {"tail": dict(zip(names, map(float, tail))),
+                                       "avg": dict(zip(names, map(float, avg)))}
+        a2a_here = pm[3] + pm[2]
         res["paper_metrics_ms"] = {
-            "token_processing_tail": float(tail[3]), "token_processing_avg": float(avg[3]),
-            "all_to_all_tail": float(max_over_ranks([pm[2] + pm[4]])[0]),
-            "all_to_all_avg": float(mean_over_ranks([pm[2] + pm[4]])[0])}
+            "token_processing_tail": float(tail[1]), "token_processing_avg": float(avg[1]),
+            "all_to_all_tail": float(max_over_ranks([a2a_here])[0]),
+            "all_to_all_avg": float(mean_over_ranks([a2a_here])[0]),
+            "note": "phases serialised (sync + barrier between them); the overlapped step is `ms_per_step`"}
         if N > 1:
-            # NVLink traffic this rank drives per phase: its remote routed rows x 2H bytes
-            # (dispatch pushes them to the hosting ranks, combine pulls them back); with
-            # tp > 1 every row goes to the tp ranks of its group (one of them may be us)
+            # NVLink bytes this rank drives: its remote routed rows x 2H out in the
+            # dispatch (tp > 1: to every TP rank of the group), and the same rows back
+            # in the combine (pulled by K8, or -- fused combine -- pushed by the hosting
+            # ranks' K6 epilogues, so the return leaves this rank as the rows IT hosts)
             sent = sum(int(info.send_counts[g]) * (tp if g != grp else tp - 1) for g in range(G))
-            nv_bytes = sent * 2 * H
-            bw = [nv_bytes / (pm[2] * 1e-3) / 1e9, nv_bytes / (pm[4] * 1e-3) / 1e9]
-            res["nvlink"] = {"remote_bytes_per_phase_rank0": nv_bytes,
-                             "dispatch_GBps_rank0": float(bw[0]), "combine_GBps_rank0": float(bw[1]),
-                             "peak_GBps": 900.0, "measured_peer_copy_GBps": 770.0,
-                             "note": "per direction; phase times include the count exchange and, for "
-                                     "combine, waiting for the slowest rank's expert FFN"}
+            hosted_remote = int(info.recv_counts[grp]) - int(info.send_counts[grp])
+            fused = os.environ.get("MOE_FUSED_COMBINE")
+            fused = (Fl <= 8192) if fused is None else fused != "0"
+            out_b = sent * 2 * H
+            ret_b = (hosted_remote if fused else sent) * 2 * H
+            push_ms = float(pm[4])
+            ret_ms = float(pm[6] if fused else pm[2])
+            res["nvlink"] = {
+                "dispatch_push_bytes": out_b, "dispatch_push_ms": push_ms,
+                "dispatch_push_GBps": out_b / (push_ms * 1e-3) / 1e9,
+                "combine_return_bytes": ret_b, "combine_return_ms": ret_ms,
+                "combine_return_GBps": ret_b / (ret_ms * 1e-3) / 1e9 if ret_ms > 0 else None,
+                "combine_mode": "fused into K6 (window = K6)" if fused else "pulled by K8 (window = combine)",
+                "peak_GBps": 900.0, "measured_peer_copy_GBps": 770.0,
+                "note": "rank 0, per direction, serialised phases; windows from the library's timeline events"}
         results[name] = res
 
     # ---- the 32-layer routing-statistics profiling pass: per layer
@@ -602,8 +634,9 @@ def run_ours(args):
                 "value": min(args.cpu_tokens, T) * len(times) / sum(times), "unit": "tokens/s", "cores": cores,
                 "kind": "oracle",
                 "sample": f"{args.cpu_reps} x {min(args.cpu_tokens, T)} random tokens of the same workload through "
-                          f"oracle.layer.layer_ep (float64 numpy, G=1); weights pre-converted bf16->float64 "
-                          f"outside the timed region; total {sum(times):.1f} s"}
+                          f"oracle.layer.layer_ep (float64 numpy, G=1: the expert matmuls are numpy float64 "
+                          f"BLAS calls on {cores} threads, the rest plain numpy); weights pre-converted "
+                          f"bf16->float64 outside the timed region; total {sum(times):.1f} s"}
         print(json.dumps(line), flush=True)
     if N > 1:
         dist.barrier()
@@ -643,8 +676,8 @@ def run_reference(args):
                        "zipf_s": args.zipf_s},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                              "sample": f"each step = {args.ref_tokens} random tokens of the workload through "
-                                       f"oracle.layer.layer_ep{'_tp' if tp > 1 else ''} (float64 numpy) on the host "
-                                       f"cores"},
+                                       f"oracle.layer.layer_ep{'_tp' if tp > 1 else ''} (float64 numpy; the expert "
+                                       f"matmuls are numpy float64 BLAS calls on {cores} threads)"},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     del world

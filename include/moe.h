@@ -114,12 +114,31 @@ moe_status moe_get_unique_id(uint8_t out[128]);
  * <= 256 routed rows per expert -- they run the GEMM on 128-row tiles).
  * uid: host, 128 bytes from moe_get_unique_id, or NULL when world == 1. */
 moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out);
-moe_status moe_ctx_destroy(moe_ctx_t ctx);               /* collective when world > 1 */
+/* Single-process group: create the n contexts of an n-rank EP group inside this
+ * process (out: host array of n handles; rank r = out[r]).  Same semantics as n
+ * processes calling moe_ctx_create with world = n, rank = r and a2a_mode =
+ * MOE_A2A_P2P, except that the peer tables hold the other contexts' device
+ * pointers directly -- no CUDA IPC, no NCCL (moe_stats_allreduce* return
+ * MOE_ERR_UNSUPPORTED).  devices: host int32 [n], the device of each rank, or
+ * NULL = cfg->device for all; ranks on different devices use peer access.
+ * Several ranks may share one device (e.g. an EP group emulated with the real
+ * multi-rank data plane on one GPU): each then runs its persistent GEMM grids on
+ * (SMs - 16) / (ranks on the device) SMs, so every rank's kernels co-reside.
+ * cfg->world and cfg->rank are ignored; cfg->virtual_ranks must be <= 1.  Every
+ * rank's calls are issued on its own stream(s); a rank's collective calls may be
+ * issued from one host thread in rank order (no call blocks on a peer) -- except
+ * moe_dispatch with info != NULL, moe_ctx_sync and the debug / timing reads,
+ * which synchronise and so must come after every rank's calls they depend on. */
+moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t* devices, moe_ctx_t* out);
+/* Collective when world > 1 (starts with a barrier over the group, so no peer
+ * still reads this rank's mapped buffers).  A single-process group's context
+ * synchronises every device of the group first. */
+moe_status moe_ctx_destroy(moe_ctx_t ctx);
 moe_status moe_ctx_sync(moe_ctx_t ctx);                   /* sync the last stream; surfaces MOE_ERR_DEVICE */
 const char* moe_status_str(moe_status s);
 const char* moe_last_error(moe_ctx_t ctx);                /* "" if none; ctx may be NULL */
 int32_t moe_abi_version(void);                            /* MOE_ABI_VERSION */
-#define MOE_ABI_VERSION 2   /* 2: moe_config.tp */
+#define MOE_ABI_VERSION 3   /* 2: moe_config.tp; 3: device expert_to_rank, moe_expert_ffn n_w, groups */
 
 /* ---- a1: gating (G1, G2, G3) -------------------------------------
  * For each token t: idx[t][0..k-1] = the k largest logits[t][.] in descending
@@ -154,9 +173,16 @@ moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coa
 
 /* ---- a3-a5: dispatch (G7, G8, G9, G13, G14) ---
  * x: bf16 [T][H] (this process's tokens); idx: int32 [T][k] from moe_route.
- * expert_to_rank: HOST int32 [E], values in [0, G/tp) (the placement input: the
- * EP rank -- with tp > 1 the EP group -- hosting each expert; a rank may host 0
- * experts).  Builds the stable send order (key P[e], e, t), the
+ * expert_to_rank: DEVICE int32 [E], values in [0, G/tp) (the placement input --
+ * "the custom expert-to-GPU mapping is loaded and applied", P:L515-519 -- the EP
+ * rank, with tp > 1 the EP group, hosting each expert; a rank may host 0
+ * experts).  It is read by the kernels this call enqueues (stream order), so a
+ * per-layer placement is just another device array: no host synchronisation,
+ * and a multi-layer chain with per-layer placements can be captured in one CUDA
+ * graph.  Its values are validated on the device: one outside [0, G/tp) latches
+ * MOE_ERR_DEVICE (and is treated as 0); MOE_A2A_NCCL, which reads the placement
+ * on the host anyway, returns MOE_ERR_INVALID_ARG from this call instead.
+ * Builds the stable send order (key P[e], e, t), the
  * expert-major receive layout (e ascending on g, then source s, then t; each
  * expert segment padded to the GEMM M tile) and moves every routed row to the rank
  * hosting its expert.  Collective when world > 1 (NCCL mode synchronises the
@@ -165,13 +191,14 @@ moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coa
  * synchronises `stream` and fills it.  A hash of expert_to_rank travels with the
  * counts and every rank checks that all ranks dispatched with the same placement:
  * MOE_A2A_P2P latches MOE_ERR_DEVICE on the device (reported by the next
- * synchronising call); MOE_A2A_NCCL returns MOE_ERR_DEVICE from this call.
+ * synchronising call); MOE_A2A_NCCL all-gathers the maps themselves and returns
+ * MOE_ERR_DEVICE from this call.
  * CUDA graphs: a whole layer (moe_route .. moe_combine) may be captured and
  * replayed on a stream (not in MOE_A2A_NCCL mode, whose dispatch reads the
  * counts on the host).  In MOE_A2A_P2P mode the flag epoch lives on the device
  * and advances once per dispatch, so every rank must replay its graph the same
  * number of times, in the same order as its other collective calls; the
- * placement must not change between capture and replay. */
+ * captured placement array is read at replay time. */
 moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
                         const int32_t* expert_to_rank, moe_dispatch_info* info,
                         moe_stream_t stream);
@@ -181,7 +208,11 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
  *   h = bf16( silu(X_e W1_e^T) * (X_e W3_e^T) ),  Y_e = bf16( h W2_e^T )
  * with fp32 accumulation on tcgen05 tensor cores.  w13: bf16 packed
  * [n_w][2F][H] (see moe_pack_w13), w2: bf16 [n_w][H][F]; n_w experts in
- * ascending global id: the hosted experts (real mode) or all E (virtual).
+ * ascending global id: the experts the last dispatch's placement hosts here
+ * (real mode; 0 allowed, w13/w2 may then be NULL) or all E (virtual: n_w must
+ * be E).  Since the placement is a device array, n_w is checked on the device:
+ * a count that differs from the hosted experts latches MOE_ERR_DEVICE (weight
+ * rows past n_w read as zeros, no out-of-bounds access).
  * tp > 1, real ranks: this rank's slice q = rank % tp only, F_q = F / tp:
  *   w13 = moe_pack_w13(W1[:, qF_q:(q+1)F_q, :], W3[same rows], n_w, F_q, H) [n_w][2F_q][H],
  *   w2  = W2[:, :, qF_q:(q+1)F_q] made contiguous                          [n_w][H][F_q];
@@ -194,7 +225,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
  * Collective in MOE_A2A_P2P mode: every rank calls it after moe_dispatch, also
  * a rank hosting no expert (w13/w2 may then be NULL) -- it raises the flag the
  * peers' moe_combine waits for. */
-moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2,
+moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2, int32_t n_w,
                           moe_stream_t stream);
 
 /* ---- a7-a8: combine (G4) -------------------------------------------------

@@ -17,7 +17,6 @@ constexpr int kMaxExperts = 256;
 constexpr int kMaxK = 16;
 constexpr int kMaxWorld = 64;
 constexpr int kMaxTP = 8;            // tensor-parallel ranks per EP group
-constexpr int kPushChunk = 32;       // rows per k_push work unit (one expert's send-order run)
 
 // Device error word bits (latched; surfaced by moe_ctx_sync as MOE_ERR_DEVICE).
 constexpr int kErrBadExpert = 1;
@@ -25,6 +24,8 @@ constexpr int kErrCapacity = 2;
 constexpr int kErrTimeout = 4;  // a P2P peer flag never arrived
 constexpr int kErrPlacement = 8;  // ranks passed different expert_to_rank maps to one dispatch
 constexpr int kErrNaN = 16;       // a router logit is NaN (reading G3: logits are finite)
+constexpr int kErrBadRank = 32;   // an expert_to_rank value outside [0, G / tp)
+constexpr int kErrWeights = 64;   // moe_expert_ffn got weights for n_w experts, the placement hosts another count
 constexpr unsigned long long kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -53,11 +53,13 @@ struct GemmCfg {
   // a 2 KB buffer (dense 64-byte rows) and one lane stores each chunk with a
   // TMA 2D store (async: the warp moves on to the next TMEM chunk while the
   // copy engine writes the rows).  Measured: the output stores were costing the
-  // GEMMs ~10% (profiles/r1_v17_*).  MOE_EPI_LSU builds the LSU variant instead
-  // (pitch 80 B, 64-byte row segments stored by all lanes).
-  static constexpr int EPI_PITCH = 80;
+  // GEMMs ~10% (profiles/r1_v17_*); an LSU variant of the staged stores measured
+  // equal and was removed.
+  // (one 2 KB buffer per warp: 32 dense 64-byte rows, 64-byte swizzled -- see
+  // epi_store_chunk_tma; a second buffer would push K5 past the shared memory that
+  // lets a k_scatter CTA co-reside with it in P2P mode)
   static constexpr int EPI_BUF = 32 * 64;
-  static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 4 * 32 * EPI_PITCH;
+  static constexpr int STAGING = FUSED ? 4 * 32 * STAGE_PITCH : 4 * EPI_BUF;
   static constexpr int BUDGET = (FUSED ? kSmemBudget : kSmemBudget + 10 * 1024) - STAGING;
   static constexpr int STAGES = (BUDGET / STAGE_BYTES) > 8 ? 8 : (BUDGET / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
@@ -124,66 +126,47 @@ __device__ __forceinline__ void decode_tile(const SegSmem& sg, int ntn, int tile
 }
 
 // One warp's 32 rows x 32 bf16 columns (lane = row, packed = its 64 bytes) ->
-// D[wrow0 + r][col0 .. col0 + 32): staged in smem (pitch 80 B, conflict-free),
-// then written as 64-byte row segments, 8 rows per store instruction.
-// TMA variant: the chunk goes to the warp's 2 KB staging buffer; lane 0 issues the
-// store after every lane wrote its row and fenced it for the async proxy.  (One
-// buffer per warp: two would push K5 past the shared memory that lets a k_scatter
-// CTA co-reside with it in P2P mode.)
-__device__ __forceinline__ void epi_store_chunk_tma(uint8_t* stg, int n, const uint32_t (&packed)[16],
+// D[wrow0 + r][col0 .. col0 + 32): the chunk goes to the warp's 2 KB staging
+// buffer (512-byte aligned) in the TMA 64-byte swizzle -- 16-byte granule g of
+// row r sits at granule g ^ ((r >> 1) & 3) -- so each 16-byte store instruction
+// of the warp hits 8 distinct bank groups per 8 lanes (4 wavefronts, no
+// conflicts; the unswizzled lane * 64 layout was a 16-20-way conflict, ncu
+// round 1); lane 0 issues the TMA 2D store after every lane wrote its row and
+// fenced it for the async proxy.
+__device__ __forceinline__ void epi_store_chunk_tma(uint8_t* stg, const uint32_t (&packed)[16],
                                                     const CUtensorMap* tmD, int wrow0, int col0, int lane) {
-  (void)n;
   uint8_t* buf = stg;
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous chunk was read
   __syncwarp();
   uint4* mine = reinterpret_cast<uint4*>(buf + lane * 64);
+  const int sw = (lane >> 1) & 3;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) mine[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+  for (int i = 0; i < 4; ++i)
+    mine[i ^ sw] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
-#ifndef MOE_EPI_NO_EVICT_FIRST
     tma_store_2d_hint(tmD, buf, col0, wrow0, l2_evict_first_policy());
-#else
-    tma_store_2d(tmD, buf, col0, wrow0);
-#endif
     bulk_commit();
   }
 }
 
-__device__ __forceinline__ void epi_store_chunk(uint8_t* stg, const uint32_t (&packed)[16], uint16_t* D, int ldd,
-                                                long long wrow0, long long col0, int lane) {
-#ifdef MOE_EPI_NOSTORE  // timing experiment only (wrong results): no output stores
-  if (lane < 0) D[0] = (uint16_t)packed[0];
-  return;
-#endif
-#ifdef MOE_EPI_DIRECT  // A/B builds: the lane writes its own row's 64 bytes directly
-  uint4* dst = reinterpret_cast<uint4*>(D + (wrow0 + lane) * ldd + col0);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) dst[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-  return;
-#endif
-  uint4* mine = reinterpret_cast<uint4*>(stg + lane * 80);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) mine[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int idx = j * 32 + lane;        // (row, 16-byte piece) = (idx / 4, idx % 4)
-    const int r = idx >> 2, piece = idx & 3;
-    const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 80 + piece * 16);
-    *reinterpret_cast<uint4*>(D + (wrow0 + r) * ldd + col0 + piece * 8) = v;
-  }
-  __syncwarp();
+// SwiGLU of one output: silu(g) * u = g * u / (1 + e^-g) (reading G5), with the
+// MUFU exp2 and reciprocal (relative error ~1e-7, far below the bf16 rounding
+// that follows) instead of an IEEE division with its slow-path branch.
+__device__ __forceinline__ float silu_mul(float g, float u) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + __expf(-g)));
+  return g * u * r;
 }
 
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint16_t* __restrict__ D, int ldd, const int32_t* __restrict__ seg_meta, int E, int N, int K,
-                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int pf,
-                   int tile_ahead, int ksplit, float* __restrict__ part, long long part_stride,
-                   const __grid_constant__ CUtensorMap tmD) {
+                   int group_m, const SrcWait sw, int* err, unsigned* sched, const FusedRet fr, int ksplit,
+                   float* __restrict__ part, long long part_stride, const __grid_constant__ CUtensorMap tmD,
+                   int n_w) {
   using C = GemmCfg<BN, CG, FUSED>;
   static_assert(!(FUSED && SWIGLU), "the fused combine applies to the down projection (K6) only");
   extern __shared__ uint8_t smem_raw[];
@@ -215,6 +198,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // ---- segment table -> smem (tile prefix over segments)
   if (threadIdx.x == 0) {
     const int nseg = seg_meta[0];
+    // the weights hold n_w experts; the placement of the last dispatch hosts nseg here
+    // (a mismatch is a caller error: latched, and the TMA zero-fills rows past n_w)
+    if (blockIdx.x == 0 && nseg != n_w) atomicOr(err, kErrWeights);
     sg.nseg = nseg;
     int accA = 0, accB = 0;
     for (int i = 0; i < nseg; ++i) {
@@ -314,23 +300,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int seq = 0;
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
-      int ready_seg = -1;            // (per-segment flags: the segment `ready` refers to)
       // P2P: this dispatch's flag value (written by k_layout earlier on the stream)
       const unsigned epoch = sw.flags != nullptr ? *(volatile const unsigned*)sw.epoch_ptr : 0u;
-      // (tile_ahead) the next tile id may be fetched one tile ahead, so the global
-      // atomic's latency overlaps this tile's loads; off by default (measured slower)
-      int next_tile = (leader && tile_ahead) ? (int)atomicAdd(sched, 1u) : 0;
       while (true) {
         int tile;
         if (leader) {
           const int slot = seq % kSchedRing;
           mbar_wait_cluster(&sempty[slot], (uint32_t)(((seq / kSchedRing) & 1) ^ 1));
-          if (tile_ahead) {
-            tile = next_tile;
-            if (tile < total_tiles) next_tile = (int)atomicAdd(sched, 1u);
-          } else {
-            tile = (int)atomicAdd(sched, 1u);
-          }
+          tile = (int)atomicAdd(sched, 1u);
           sched_tile[slot] = tile;
           if constexpr (CG == 2) {
             st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)tile);
@@ -355,12 +332,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // those generic-proxy arrivals before the TMA (async proxy) reads
           const int32_t* ss = sw.seg_src + (long long)seg * sw.G * 3;
           bool waited = false;
-          if (sw.per_seg && seg != ready_seg) {
-            ready = 0;
-            ready_seg = seg;
-          }
-          const unsigned* fl = sw.per_seg ? sw.flags + seg : sw.flags;
-          const int fstride = sw.per_seg ? 256 : 1;  // SigBlock::flag_seg[s][pos] / flag_data[s]
           for (int s = 0; s < sw.G; ++s) {
             if (s == sw.me || ((ready >> s) & 1ull)) continue;
             const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
@@ -368,7 +339,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const unsigned long long t0 = globaltimer_ns();
             unsigned v;
             do {
-              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl + s * fstride) : "memory");
+              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sw.flags + s) : "memory");
               if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
                 atomicOr(err, kErrTimeout);
                 break;
@@ -379,17 +350,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
         }
-        // L2 prefetch `pf` k-blocks ahead of the loads: the first cluster to touch a
-        // weight tile would otherwise stall on DRAM latency for each of its k-blocks
-        for (int kb = kb_lo; kb < min(kb_lo + pf, kb_hi); ++kb) {
-          tma_prefetch_l2_2d(&tmA, kb * BK, a_row);
-          tma_prefetch_l2_2d(&tmB, kb * BK, b_row);
-        }
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
-          if (pf > 0 && kb + pf < kb_hi) {
-            tma_prefetch_l2_2d(&tmA, (kb + pf) * BK, a_row);
-            tma_prefetch_l2_2d(&tmB, (kb + pf) * BK, b_row);
-          }
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -487,7 +448,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                  __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
         }
       } else if constexpr (SWIGLU) {
-        uint8_t* stg = staging + (size_t)(warp - 2) * 32 * C::EPI_PITCH;
+        uint8_t* stg = staging + (size_t)(warp - 2) * C::EPI_BUF;
         const long long wrow0 = arow + (int)crank * 128 + q * 32;  // first row of this warp
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
@@ -500,15 +461,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int i = 0; i < 16; ++i) {
             const float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
             const float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
-            const float h0 = g0 / (1.0f + __expf(-g0)) * u0;
-            const float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+            const float h0 = silu_mul(g0, u0), h1 = silu_mul(g1, u1);
             packed[i] = pack_bf16x2(h0, h1);
           }
-#ifndef MOE_EPI_LSU
-          epi_store_chunk_tma(stg, c / 32, packed, &tmD, (int)wrow0, nt * (BN / 2) + c, lane);
-#else
-          epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * (BN / 2) + c, lane);
-#endif
+          epi_store_chunk_tma(stg, packed, &tmD, (int)wrow0, nt * (BN / 2) + c, lane);
         }
       } else if constexpr (FUSED) {
         // Fused combine: the row belongs to source s (rows of s are contiguous in the
@@ -558,7 +514,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           bulk_commit();
         }
       } else {
-        uint8_t* stg = staging + (size_t)(warp - 2) * 32 * C::EPI_PITCH;
+        uint8_t* stg = staging + (size_t)(warp - 2) * C::EPI_BUF;
         const long long wrow0 = arow + (int)crank * 128 + q * 32;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -568,11 +524,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t packed[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-#ifndef MOE_EPI_LSU
-          epi_store_chunk_tma(stg, c / 32, packed, &tmD, (int)wrow0, nt * BN + c, lane);
-#else
-          epi_store_chunk(stg, packed, D, ldd, wrow0, (long long)nt * BN + c, lane);
-#endif
+          epi_store_chunk_tma(stg, packed, &tmD, (int)wrow0, nt * BN + c, lane);
         }
       }
       if (FUSED && ksplit > 1) {  // (never launched: split-K is not combined with the fused combine)
@@ -639,7 +591,7 @@ int gemm_b_box_rows(int N, bool swiglu, int cg) { return gemm_block_n(N, swiglu)
 
 template <int BN, bool SWIGLU, int CG, bool FUSED = false>
 static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta, int E,
-                               int N, int K, int num_sms, const SrcWait& sw, int* err, unsigned* sched,
+                               int n_w, int N, int K, int num_sms, const SrcWait& sw, int* err, unsigned* sched,
                                const FusedRet& fr, cudaStream_t s, int ksplit, float* part, long long part_stride,
                                const void* tmD) {
   using C = GemmCfg<BN, CG, FUSED>;
@@ -683,30 +635,19 @@ static cudaError_t launch_impl(const void* tmA, const void* tmB, uint16_t* D, in
   if (group_m < 1) group_m = 1;
   if (group_m > 64) group_m = 64;
   if (env_group != 0) group_m = env_group;
-  static int pf = -1;  // L2 prefetch distance in k-blocks (MOE_GEMM_PREFETCH, tuning)
-  if (pf < 0) {
-    const char* env = getenv("MOE_GEMM_PREFETCH");
-    pf = env ? atoi(env) : 0;
-    if (pf < 0) pf = 0;
-  }
-  static int ahead = -1;  // MOE_GEMM_TILE_AHEAD=1: fetch tile ids one tile ahead (tuning)
-  if (ahead < 0) {
-    const char* env = getenv("MOE_GEMM_TILE_AHEAD");
-    ahead = (env && atoi(env) != 0) ? 1 : 0;
-  }
   return cudaLaunchKernelEx(&cfg, kern, a, b, D, ldd, seg_meta, E, N, K, group_m, sw, err,
-                            sched, fr, pf, ahead, ksplit, part, part_stride, dmap);
+                            sched, fr, ksplit, part, part_stride, dmap, n_w);
 }
 
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
+                                int E, int n_w, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
                                 unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit, float* part,
                                 long long part_stride, const void* tmD) {
   const int bn = gemm_block_n(N, swiglu);
   if (ksplit < 1) ksplit = 1;
   const bool fused = fr.enabled && !swiglu;
 #define MOE_GO(BN_, SW_, CG_, FU_) \
-  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, N, K, num_sms, sw, err, sched, fr, s, ksplit, part, \
+  launch_impl<BN_, SW_, CG_, FU_>(tmA, tmB, D, ldd, seg_meta, E, n_w, N, K, num_sms, sw, err, sched, fr, s, ksplit, part, \
                                   part_stride, tmD)
 #define MOE_GO2(BN_, CG_) (fused ? MOE_GO(BN_, false, CG_, true) : MOE_GO(BN_, false, CG_, false))
   if (cg == 2) {
@@ -754,50 +695,6 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__
   }
 }
 
-// Split-K reduction of the gate/up GEMM (K5): the packed columns of block b are
-// [b*2B, b*2B+B) gate and [b*2B+B, b*2B+2B) up (B = BN/2, moe_pack_w13); the slice
-// sums feed the same SwiGLU as K5's epilogue: h = bf16(silu(g) * u).
-__global__ void __launch_bounds__(256) k_splitk_reduce_swiglu(const float* __restrict__ part, long long part_stride,
-                                                              int S, const int32_t* __restrict__ seg_meta, int E,
-                                                              int F, int B, int tile_m, uint16_t* __restrict__ D,
-                                                              int ldd) {
-  const int nseg = seg_meta[0];
-  const int f4 = F / 4;
-  const int N = 2 * F;
-  for (int i = 0; i < nseg; ++i) {
-    const long long r0 = seg_meta[1 + i];
-    const int rows = seg_meta[1 + E + i];
-    const long long n = (long long)((rows + tile_m - 1) / tile_m) * tile_m * f4;
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
-      const long long row = r0 + p / f4;
-      const int f = (int)(p % f4) * 4;
-      const int gc = (f / B) * 2 * B + f % B;
-      const float* src = part + row * N + gc;
-      float4 g = *reinterpret_cast<const float4*>(src);
-      float4 u = *reinterpret_cast<const float4*>(src + B);
-      for (int sl = 1; sl < S; ++sl) {
-        const float4 a = *reinterpret_cast<const float4*>(src + sl * part_stride);
-        const float4 b = *reinterpret_cast<const float4*>(src + sl * part_stride + B);
-        g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
-        u.x += b.x; u.y += b.y; u.z += b.z; u.w += b.w;
-      }
-      const float h0 = g.x / (1.0f + __expf(-g.x)) * u.x, h1 = g.y / (1.0f + __expf(-g.y)) * u.y;
-      const float h2 = g.z / (1.0f + __expf(-g.z)) * u.z, h3 = g.w / (1.0f + __expf(-g.w)) * u.w;
-      uint2 o;
-      o.x = pack_bf16x2(h0, h1);
-      o.y = pack_bf16x2(h2, h3);
-      *reinterpret_cast<uint2*>(D + row * ldd + f) = o;
-    }
-  }
-}
-
-cudaError_t launch_splitk_reduce_swiglu(const float* part, long long part_stride, int S, const int32_t* seg_meta,
-                                        int E, int F, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s) {
-  const int B = gemm_block_n(2 * F, true) / 2;
-  k_splitk_reduce_swiglu<<<2 * num_sms, 256, 0, s>>>(part, part_stride, S, seg_meta, E, F, B, 128 * cg, D, ldd);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
                                  int N, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s) {
   k_splitk_reduce<<<2 * num_sms, 256, 0, s>>>(part, part_stride, S, seg_meta, E, N, 128 * cg, D, ldd);
@@ -825,11 +722,11 @@ bool make_tmap_store_2d(void* tmap_out, const void* base, uint64_t rows, uint64_
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {32, 32};  // one epilogue chunk: 32 rows x 32 bf16 (dense 64-byte rows)
+  cuuint32_t box[2] = {32, 32};  // one epilogue chunk: 32 rows x 32 bf16 (64-byte rows, 64-byte swizzle)
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(reinterpret_cast<CUtensorMap*>(tmap_out), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -845,6 +742,26 @@ bool make_tmap_2d_ld(void* tmap_out, const void* base, uint64_t rows, uint64_t c
                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool SWIGLU, int CG, bool FUSED = false>
+static void preload_one() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, (const void*)k_grouped_gemm<BN, SWIGLU, CG, FUSED>);
+  cudaFuncSetAttribute(k_grouped_gemm<BN, SWIGLU, CG, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       GemmCfg<BN, CG, FUSED>::SMEM);
+}
+
+void preload_gemm_kernels() {
+#define MOE_PL(CG_)                                                                                        \
+  preload_one<256, true, CG_>(), preload_one<128, true, CG_>(), preload_one<256, false, CG_>(),           \
+      preload_one<128, false, CG_>(), preload_one<64, false, CG_>(), preload_one<256, false, CG_, true>(), \
+      preload_one<128, false, CG_, true>(), preload_one<64, false, CG_, true>()
+  MOE_PL(1);
+  MOE_PL(2);
+#undef MOE_PL
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, (const void*)k_splitk_reduce);
 }
 
 }  // namespace moe

@@ -18,8 +18,6 @@ struct SigBlock {
   unsigned flag_data[64];     // flag_data[s] = epoch once every row s sends here landed
   unsigned flag_y[64];        // flag_y[g] = epoch once rank g's expert outputs are ready
   unsigned phash[64];         // phash[s] = hash of the placement source s dispatched with
-  unsigned flag_seg[64][256]; // flag_seg[s][pos] = epoch once source s's rows of this rank's
-                              // pos-th hosted expert landed (slot-ordered push, k_push)
 };
 
 // Dispatch plan arguments shared by K2/K3/K8 (dispatch.cu).
@@ -45,7 +43,8 @@ struct PlanArgs {
 
 // Device-side plan state (allocated by the context).
 struct PlanBuffers {
-  const int32_t* P;      // [E] placement
+  const int32_t* P_in;   // [E] the caller's expert_to_rank of this dispatch (device)
+  int32_t* P;            // [E] context copy, validated by k_layout (read by the later kernels)
   int32_t* tile_hist;    // [n_tiles][E]
   int32_t* tile_base;    // [n_tiles][E]  within-source exclusive prefix
   int32_t* cnt_local;    // [V][E]
@@ -69,25 +68,16 @@ struct PlanBuffers {
   // tp > 1: the tp partial outputs of one item live part_stride uint4 apart (virtual
   // mode: the expert-output buffers of the slices; fused combine: the return buffers)
   long long part_stride;
-  // slot-ordered P2P push (k_push): inverse of cslot_of_item, per-expert pushed-row
-  // counters, and the work table built by k_layout:
-  //   push_work[0] = items, push_work[1] = chunks, then per item (e, first chunk, pos of e
-  //   among its EP group's experts); items ordered (pos, destination group rotated by rank)
-  int32_t* item_of_slot;
-  int32_t* done_rows;
-  int32_t* push_work;
 };
 
 // K5 per-tile arrival waits (P2P overlap): the producer waits only for the source
 // ranks whose rows a tile reads; tiles holding only this rank's own rows run first.
 struct SrcWait {
-  const unsigned* flags;          // per_seg ? SigBlock::flag_seg [G][256] : flag_data [G] of this
-                                  // rank; nullptr = no waits (all rows local)
+  const unsigned* flags;          // SigBlock::flag_data [G] of this rank; nullptr = no waits
   const int32_t* seg_src;         // see PlanBuffers::seg_src
   int G;
   int me;
   const unsigned* epoch_ptr;      // see PlanArgs::epoch_ptr
-  int per_seg;                    // 1: wait per (source, hosted segment) (slot-ordered push)
 };
 
 // K6 epilogue redirection (fused combine, P2P mode); enabled == 0 -> plain stores.
@@ -98,22 +88,28 @@ struct FusedRet {
   int enabled;
 };
 
+// Load every kernel of the library onto the current device now (CUDA 12 loads
+// modules lazily, at a function's first launch; a first launch may wait for the
+// device's running kernels -- and in a single-process EP group a running kernel
+// can be spinning on a flag that only a later launch of this thread raises).
+void preload_route_kernels();
+void preload_dispatch_kernels();
+void preload_gemm_kernels();
+
 int plan_tiles(int T, int V);
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
 void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s);
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s);
-// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers,
-// 3 = plan arrays only (+ item_of_slot), 4 = rows hosted here only (plan already built)
+// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
                     cudaStream_t s, int max_ctas = 0);  // max_ctas > 0: persistent grid of that size
-// P2P: rows for peers in send order, chunk by chunk, raising flag_seg per (source, expert)
-// as each expert's rows complete (K5 consumes experts as they arrive).
-void launch_push(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int num_sms, cudaStream_t s);
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s);
 // P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);
 // P2P: wait until flags[0..n) >= epoch (system-scope acquire).
 void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, cudaStream_t s);
+// Latch kErrWeights unless the last layout hosts exactly n expert segments here.
+void launch_expect_nseg(const int32_t* seg_meta, int n, int* err, cudaStream_t s);
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13,
                      cudaStream_t s);
 
@@ -127,7 +123,7 @@ int pack_block(int F);
 // cg = CTAs per MMA (2: tcgen05 cta_group::2, 256-row tiles; 1: 128-row tiles for
 // small token counts); must match the segment padding of the dispatch layout.
 cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, int ldd, const int32_t* seg_meta,
-                                int E, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
+                                int E, int n_w, int N, int K, bool swiglu, int cg, int num_sms, const SrcWait& sw, int* err,
                                 unsigned* sched, const FusedRet& fr, cudaStream_t s, int ksplit = 1,
                                 float* part = nullptr, long long part_stride = 0, const void* tmD = nullptr);
 // tmD: TMA-store map of D (make_tmap_store_2d) for the plain / SwiGLU epilogues.
@@ -135,9 +131,6 @@ cudaError_t launch_grouped_gemm(const void* tmA, const void* tmB, uint16_t* D, i
 // part[slice][row][N]; launch_splitk_reduce then writes D = bf16(sum over slices).
 cudaError_t launch_splitk_reduce(const float* part, long long part_stride, int S, const int32_t* seg_meta, int E,
                                  int N, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s);
-// Same for the gate/up GEMM: h = bf16(silu(sum gate) * (sum up)), packed columns.
-cudaError_t launch_splitk_reduce_swiglu(const float* part, long long part_stride, int S, const int32_t* seg_meta,
-                                        int E, int F, int cg, uint16_t* D, int ldd, int num_sms, cudaStream_t s);
 // sched: 2 zero-initialised device counters (tile counter, exit counter) owned by the
 // caller; the kernel resets them to 0 when it completes.
 // Encode a 2D bf16 K-major tensor map [rows][cols] with box {64, box_rows}, 128B swizzle.

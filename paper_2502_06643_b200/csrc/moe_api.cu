@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -29,11 +30,13 @@ struct moe_ctx {
   std::string err;
   int64_t launches = 0;
 
-  // placement
+  // placement of the last dispatch: the caller passes it as a device array; k_layout
+  // validates it and copies it here (NCCL mode also all-gathers every rank's copy
+  // into P_all and reads it on the host with the counts)
   int32_t* P_dev = nullptr;
-  int32_t* P_pinned = nullptr;
-  std::vector<int32_t> P_host;
-  bool P_valid = false;
+  int32_t* P_all = nullptr;         // NCCL mode: [G][E]
+  int32_t* P_all_pinned = nullptr;  // [G][E] host staging
+  std::vector<int32_t> P_host;      // NCCL mode: this rank's row of P_all after the sync
 
   // plan workspaces
   int max_tiles = 0;
@@ -46,8 +49,6 @@ struct moe_ctx {
   int32_t* row_of_item = nullptr;
   int* err_dev = nullptr;
   int32_t* cnt_pinned = nullptr;  // host copy of cnt_all (NCCL mode / debug)
-  uint32_t* phash_dev = nullptr;  // NCCL mode: [G] all-gathered placement hashes + [1] this rank's
-  uint32_t* phash_pinned = nullptr;  // [G + 1] host staging
 
   // payload buffers
   int64_t cap_rows = 0;      // receive-layout rows (padded)
@@ -104,22 +105,24 @@ struct moe_ctx {
   uint16_t** ret_table = nullptr;       // device [G]
   bool ffn_fused = false;               // the last expert FFN already returned its rows
   // P2P overlap: rows for peers are pushed on a side stream while K5 starts on
-  // this rank's own rows (fork after the layout kernel, join in combine)
+  // this rank's own rows (fork after the layout kernel, join in combine).  (A
+  // send-order push with per-(source, expert) arrival flags measured slower at E64
+  // 4EP -- 6.87 vs 6.64 ms, round 1 -- and was removed.)
   cudaStream_t side = nullptr;
-  // MOE_P2P_PUSH=slot: send-order push with per-(source, expert) arrival flags (k_push).
-  // Measured slower than the token-tile scatter at E64 4EP (6.87 vs 6.64 ms: the
-  // per-chunk system fences drain the NVLink pipeline and the push CTAs slow K5),
-  // so the default is the token-tile scatter with whole-source flags.
-  bool push_slot = false;
   // CTAs of the peers'-rows scatter that overlaps K5 (persistent grid; 0 = one per
   // tile x column slice).  32 CTAs still fill NVLink and leave the other SMs to
   // K5: D5 4EP step 6.24 ms vs 6.73 (one CTA per tile), 6.53 (16), 6.28 (64),
   // 6.59 (128) in one run (profiles/r1_v13_timeline_ctas_*); Mixtral 4EP unchanged.
   // MOE_SCATTER_CTAS overrides.
   int remote_ctas = 32;
-  int32_t* item_of_slot = nullptr;      // [max_tokens * k]
-  int32_t* done_rows = nullptr;         // [E]
-  int32_t* push_work = nullptr;         // [2 + 3E]
+  // single-process group (moe_ctx_create_group): every rank's context lives in this
+  // process; the peer tables hold the other contexts' device pointers directly (no
+  // IPC, no NCCL).  shared_dev: another rank of the group runs on the same device --
+  // the persistent grids are capped so every rank's kernels co-reside, and no kernel
+  // with more than one CTA spins on a peer flag.
+  bool local_group = false;
+  bool shared_dev = false;
+  std::shared_ptr<std::vector<int>> group_devices;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // the same pair for layers captured into a CUDA graph (an event recorded inside a
   // capture must not be waited on by eager work afterwards); cur_join = the join
@@ -129,7 +132,6 @@ struct moe_ctx {
   // last dispatch
   bool have_plan = false;
   int last_T = 0, last_k = 0, last_tiles = 0;
-  int n_hosted = 0;
   std::vector<int32_t> cnt_host;  // [G][E] (NCCL mode)
 };
 
@@ -171,6 +173,7 @@ static void tl_rec(moe_ctx_t c, int j, cudaStream_t s) {
 
 static PlanBuffers plan_buffers(moe_ctx_t c) {
   PlanBuffers b;
+  b.P_in = nullptr;  // set by moe_dispatch
   b.P = c->P_dev;
   b.tile_hist = c->tile_hist;
   b.tile_base = c->tile_base;
@@ -193,9 +196,6 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.cslot_of_item = c->cslot_of_item;
   b.ret_local = reinterpret_cast<const uint4*>(c->retbuf);
   b.part_stride = c->virt ? c->cap_rows * c->H / 8 : c->send_rows * c->H / 8;
-  b.item_of_slot = c->item_of_slot;
-  b.done_rows = c->done_rows;
-  b.push_work = c->push_work;
   return b;
 }
 
@@ -319,10 +319,9 @@ static moe_status layout_host_impl(int32_t E, int32_t G, const int32_t* P, const
   return MOE_OK;
 }
 
-moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out) {
+// Configuration checks shared by moe_ctx_create and moe_ctx_create_group.
+static moe_status check_cfg(const moe_config& c) {
   moe_ctx_t ctx = nullptr;
-  if (!cfg || !out) return fail(ctx, MOE_ERR_INVALID_ARG, "cfg/out is NULL");
-  const moe_config& c = *cfg;
   if (c.hidden <= 0 || c.hidden % 64) return fail(ctx, MOE_ERR_UNSUPPORTED, "hidden must be a positive multiple of 64");
   if (c.ffn <= 0 || c.ffn % 64) return fail(ctx, MOE_ERR_UNSUPPORTED, "ffn must be a positive multiple of 64");
   if (c.num_experts < 1 || c.num_experts > kMaxExperts)
@@ -336,7 +335,6 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   if (c.virtual_ranks > kMaxWorld) return fail(ctx, MOE_ERR_INVALID_ARG, "virtual_ranks > %d", kMaxWorld);
   if (c.a2a_mode != MOE_A2A_NCCL && c.a2a_mode != MOE_A2A_P2P)
     return fail(ctx, MOE_ERR_INVALID_ARG, "unknown a2a_mode %d", c.a2a_mode);
-  if (c.world > 1 && !uid) return fail(ctx, MOE_ERR_INVALID_ARG, "uid required when world > 1");
   const int tp = c.tp <= 1 ? 1 : c.tp;
   const int ranks = c.virtual_ranks > 1 ? c.virtual_ranks : c.world;
   if (tp > kMaxTP) return fail(ctx, MOE_ERR_INVALID_ARG, "tp=%d > %d", tp, kMaxTP);
@@ -344,8 +342,15 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   if (c.ffn % (64 * tp)) return fail(ctx, MOE_ERR_UNSUPPORTED, "ffn / tp must be a multiple of 64");
   if (tp > 1 && c.virtual_ranks <= 1 && c.a2a_mode != MOE_A2A_P2P)
     return fail(ctx, MOE_ERR_UNSUPPORTED, "tp > 1 on real ranks needs MOE_A2A_P2P");
+  return MOE_OK;
+}
 
-  ctx = new moe_ctx();
+// Allocate one rank's context: every workspace, the activation tensor maps.  No
+// communicator, no peer tables (moe_ctx_create / moe_ctx_create_group add those).
+// share = ranks of a single-process group on this device (1 otherwise).
+static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
+  moe_ctx_t ctx = new moe_ctx();
+  *out = ctx;
   ctx->cfg = c;
   ctx->E = c.num_experts;
   ctx->H = c.hidden;
@@ -354,26 +359,32 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
   ctx->G = ctx->virt ? c.virtual_ranks : c.world;
   ctx->V = ctx->virt ? c.virtual_ranks : 1;
   ctx->me = ctx->virt ? 0 : c.rank;
+  const int tp = c.tp <= 1 ? 1 : c.tp;
   ctx->tp = tp;
   ctx->grp = ctx->me / tp;
   ctx->tpi = ctx->me % tp;
   ctx->Fl = ctx->virt ? c.ffn : c.ffn / tp;
-  auto bail = [&](moe_status s) {
-    std::string m = ctx->err;
-    moe_ctx_destroy(ctx);
-    fail(nullptr, s, "%s", m.c_str());
-    return s;
-  };
-  if (cudaSetDevice(c.device) != cudaSuccess) {
-    fail(ctx, MOE_ERR_CUDA, "cudaSetDevice(%d) failed", c.device);
-    return bail(MOE_ERR_CUDA);
-  }
+  if (cudaSetDevice(c.device) != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "cudaSetDevice(%d) failed", c.device);
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, c.device);
   int major = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c.device);
-  if (major != 10) {
-    fail(ctx, MOE_ERR_UNSUPPORTED, "libmoe needs an sm_100 (B200) device, got compute capability %d.x", major);
-    return bail(MOE_ERR_UNSUPPORTED);
+  if (major != 10)
+    return fail(ctx, MOE_ERR_UNSUPPORTED, "libmoe needs an sm_100 (B200) device, got compute capability %d.x", major);
+  static unsigned long long preloaded = 0;  // per device
+  if (first_time_on_device(preloaded)) {
+    preload_route_kernels();
+    preload_dispatch_kernels();
+    preload_gemm_kernels();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "loading the kernels: %s", cudaGetErrorString(e));
+  }
+  if (share > 1) {
+    // ranks sharing one device: each gets an equal slice of the SMs for its persistent
+    // grids, 16 SMs stay free for the peers' row copies, so a GEMM CTA waiting for a
+    // peer's rows never blocks the kernel that delivers them
+    ctx->shared_dev = true;
+    ctx->num_sms = std::max(2, ((ctx->num_sms - 16) / share) & ~1);
+    ctx->remote_ctas = std::max(1, std::min(ctx->remote_ctas, ctx->num_sms / 2));
   }
   const int E = ctx->E, G = ctx->G, k = c.max_k;
   const int64_t Tm = c.max_tokens;
@@ -402,6 +413,7 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     return true;
   };
   bool ok = A((void**)&ctx->P_dev, sizeof(int32_t) * E) &&
+            A((void**)&ctx->P_all, sizeof(int32_t) * (size_t)G * E) &&
             A((void**)&ctx->tile_hist, sizeof(int32_t) * (size_t)ctx->max_tiles * E) &&
             A((void**)&ctx->tile_base, sizeof(int32_t) * (size_t)ctx->max_tiles * E) &&
             A((void**)&ctx->cnt_local, sizeof(int32_t) * (size_t)ctx->V * E) &&
@@ -424,51 +436,80 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
             A((void**)&ctx->cslot_base, sizeof(int32_t) * (size_t)E) &&
             A((void**)&ctx->cslot_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
             A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G) &&
-            A((void**)&ctx->item_of_slot, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
-            A((void**)&ctx->done_rows, sizeof(int32_t) * (size_t)E) &&
-            A((void**)&ctx->push_work, sizeof(int32_t) * (size_t)(2 + 3 * E)) &&
             A((void**)&ctx->epoch_dev, sizeof(unsigned));
-  if (!ok) return bail(MOE_ERR_CUDA);
+  if (!ok) return MOE_ERR_CUDA;
   cudaMemset(ctx->sig, 0, sizeof(SigBlock));
   cudaMemset(ctx->done_counter, 0, 4 * sizeof(unsigned));  // [0] scatter last-CTA, [2..3] GEMM scheduler
   cudaMemset(ctx->err_dev, 0, sizeof(int));
-  cudaMemset(ctx->done_rows, 0, sizeof(int32_t) * E);
   cudaMemset(ctx->epoch_dev, 0, sizeof(unsigned));
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
-  if (cudaMallocHost((void**)&ctx->P_pinned, sizeof(int32_t) * E) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->phash_pinned, sizeof(uint32_t) * (size_t)(G + 1)) != cudaSuccess ||
-      cudaMalloc((void**)&ctx->phash_dev, sizeof(uint32_t) * (size_t)(G + 1)) != cudaSuccess) {
-    fail(ctx, MOE_ERR_CUDA, "cudaMallocHost failed");
-    return bail(MOE_ERR_CUDA);
-  }
-  ctx->P_host.assign(E, -1);
+  if (cudaMallocHost((void**)&ctx->P_all_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess)
+    return fail(ctx, MOE_ERR_CUDA, "cudaMallocHost failed");
+  ctx->P_host.assign(E, 0);
   ctx->cnt_host.assign((size_t)G * E, 0);
   // A-operand tensor maps over the context-owned activation buffers
   if (!make_tmap_2d(ctx->tmA1, ctx->recv, ctx->cap_rows, c.hidden, 128) ||
-      !make_tmap_2d(ctx->tmA2, ctx->hbuf, ctx->cap_rows, ctx->Fl, 128)) {
-    fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
-    return bail(MOE_ERR_CUDA);
-  }
+      !make_tmap_2d(ctx->tmA2, ctx->hbuf, ctx->cap_rows, ctx->Fl, 128))
+    return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
   if (!make_tmap_store_2d(ctx->tmDh, ctx->hbuf, ctx->cap_rows, ctx->Fl, ctx->Fl) ||
-      !make_tmap_store_2d(ctx->tmDy, ctx->ybuf, ctx->cap_rows, c.hidden, c.hidden)) {
-    fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the epilogue store maps");
-    return bail(MOE_ERR_CUDA);
-  }
+      !make_tmap_store_2d(ctx->tmDy, ctx->ybuf, ctx->cap_rows, c.hidden, c.hidden))
+    return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the epilogue store maps");
   if (ctx->virt && tp > 1)
-    for (int q = 0; q < tp; ++q)
+    for (int q = 0; q < tp; ++q) {
       if (!make_tmap_store_2d(ctx->tmDys[q], ctx->ybuf + (size_t)q * ctx->cap_rows * c.hidden, ctx->cap_rows,
-                              c.hidden, c.hidden)) {
-        fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for a partial-output store map");
-        return bail(MOE_ERR_CUDA);
-      }
-  if (ctx->virt && tp > 1)
-    for (int q = 0; q < tp; ++q)
+                              c.hidden, c.hidden))
+        return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for a partial-output store map");
       if (!make_tmap_2d_ld(ctx->tmA2s[q], ctx->hbuf + (size_t)q * (c.ffn / tp), ctx->cap_rows, c.ffn / tp, c.ffn,
-                           128)) {
-        fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for an h slice");
-        return bail(MOE_ERR_CUDA);
-      }
+                           128))
+        return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for an h slice");
+    }
+  return MOE_OK;
+}
+
+// P2P mode: the side stream of the peers' row copies and its fork / join events.
+static moe_status p2p_streams(moe_ctx_t ctx) {
+  ctx->p2p = true;
+  if (const char* rc = getenv("MOE_SCATTER_CTAS")) ctx->remote_ctas = atoi(rc);
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_fork_cap, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_join_cap, cudaEventDisableTiming));
+  return MOE_OK;
+}
+
+// Upload the slot -> buffer tables.  NCCL / virtual: slot 0 = this process's receive /
+// expert-output buffers, slot 1 = the compact send / return buffers.  P2P: slot g =
+// rank g's receive / expert-output buffer, signal block and return buffer (region tpi).
+static moe_status upload_tables(moe_ctx_t ctx, std::vector<void*>& dst, std::vector<void*>& src,
+                                std::vector<void*>& sig, std::vector<void*>& ret) {
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->src_table, src.data(), sizeof(void*) * src.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->peer_sig, sig.data(), sizeof(void*) * ctx->G, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->ret_table, ret.data(), sizeof(void*) * ctx->G, cudaMemcpyHostToDevice));
+  CU(cudaDeviceSynchronize());
+  return MOE_OK;
+}
+
+moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out) {
+  moe_ctx_t ctx = nullptr;
+  if (!cfg || !out) return fail(ctx, MOE_ERR_INVALID_ARG, "cfg/out is NULL");
+  const moe_config& c = *cfg;
+  moe_status st = check_cfg(c);
+  if (st != MOE_OK) return st;
+  if (c.world > 1 && !uid) return fail(ctx, MOE_ERR_INVALID_ARG, "uid required when world > 1");
+  auto bail = [&](moe_status s) {
+    std::string m = ctx ? ctx->err : g_err;
+    moe_ctx_destroy(ctx);
+    fail(nullptr, s, "%s", m.c_str());
+    return s;
+  };
+  st = ctx_alloc(c, 1, &ctx);
+  if (st != MOE_OK) return bail(st);
+  const int G = ctx->G;
   if (!ctx->virt && G > 1) {
     ncclUniqueId id;
     memcpy(&id, uid, 128);
@@ -478,92 +519,157 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       return bail(MOE_ERR_NCCL);
     }
   }
-  // slot -> buffer tables.  NCCL / virtual: slot 0 = this process's receive /
-  // expert-output buffers, slot 1 = the compact send / return buffers.  P2P:
-  // slot g = rank g's receive / expert-output buffer, mapped through CUDA IPC
-  // (NVLink peer memory), exchanged once here over NCCL.
-  {
-    std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr), ret(G, nullptr);
-    ret[0] = ctx->retbuf;
-    dst[0] = ctx->recv;
-    dst[1] = ctx->sendbuf;
-    src[0] = ctx->ybuf;
-    src[1] = ctx->retbuf;
-    sig[0] = ctx->sig;
-    if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
-      ctx->p2p = true;
-      const char* pm = getenv("MOE_P2P_PUSH");
-      ctx->push_slot = pm && !strcmp(pm, "slot");
-      if (const char* rc = getenv("MOE_SCATTER_CTAS")) ctx->remote_ctas = atoi(rc);
-      if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->ev_fork_cap, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&ctx->ev_join_cap, cudaEventDisableTiming) != cudaSuccess) {
-        fail(ctx, MOE_ERR_CUDA, "side stream / event creation failed");
-        return bail(MOE_ERR_CUDA);
-      }
-      cudaIpcMemHandle_t h[4];
-      if (cudaIpcGetMemHandle(&h[0], ctx->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->ybuf) != cudaSuccess ||
-          cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess || cudaIpcGetMemHandle(&h[3], ctx->retbuf) != cudaSuccess) {
-        fail(ctx, MOE_ERR_CUDA, "cudaIpcGetMemHandle failed");
-        return bail(MOE_ERR_CUDA);
-      }
-      const size_t hb = sizeof(h);
-      uint8_t* dh = nullptr;
-      std::vector<uint8_t> all(hb * G);
-      if (cudaMalloc(&dh, hb * (G + 1)) != cudaSuccess ||
-          cudaMemcpy(dh + hb * G, h, hb, cudaMemcpyHostToDevice) != cudaSuccess ||
-          ncclAllGather(dh + hb * G, dh, hb, ncclUint8, ctx->comm, 0) != ncclSuccess ||
-          cudaStreamSynchronize(0) != cudaSuccess || cudaMemcpy(all.data(), dh, hb * G, cudaMemcpyDeviceToHost) != cudaSuccess) {
-        if (dh) cudaFree(dh);
-        fail(ctx, MOE_ERR_NCCL, "IPC handle exchange failed");
-        return bail(MOE_ERR_NCCL);
-      }
-      cudaFree(dh);
-      for (int g = 0; g < G; ++g) {
-        if (g == c.rank) {
-          dst[g] = ctx->recv;
-          src[g] = ctx->ybuf;
-          sig[g] = ctx->sig;
-          ret[g] = ctx->retbuf + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
-          continue;
-        }
-        const cudaIpcMemHandle_t* hg = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * g);
-        void* p[4] = {nullptr, nullptr, nullptr, nullptr};
-        for (int i = 0; i < 4; ++i) {
-          cudaError_t e = cudaIpcOpenMemHandle(&p[i], hg[i], cudaIpcMemLazyEnablePeerAccess);
-          if (e != cudaSuccess) {
-            fail(ctx, MOE_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", g, cudaGetErrorString(e));
-            return bail(MOE_ERR_CUDA);
-          }
-          ctx->ipc_opened.push_back(p[i]);
-        }
-        dst[g] = p[0];
-        src[g] = p[1];
-        sig[g] = p[2];
-        // fused combine of TP slice tpi lands in partial region tpi of the source's buffer
-        ret[g] = static_cast<uint16_t*>(p[3]) + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
-      }
-    }
-    if (cudaMemcpy(ctx->dst_table, dst.data(), sizeof(void*) * dst.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(ctx->src_table, src.data(), sizeof(void*) * src.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(ctx->peer_sig, sig.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(ctx->ret_table, ret.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
-      fail(ctx, MOE_ERR_CUDA, "pointer-table upload failed");
+  std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr), ret(G, nullptr);
+  ret[0] = ctx->retbuf;
+  dst[0] = ctx->recv;
+  dst[1] = ctx->sendbuf;
+  src[0] = ctx->ybuf;
+  src[1] = ctx->retbuf;
+  sig[0] = ctx->sig;
+  if (!ctx->virt && G > 1 && c.a2a_mode == MOE_A2A_P2P) {
+    // the peers' buffers are mapped through CUDA IPC (NVLink peer memory); the
+    // handles are exchanged once here over NCCL
+    st = p2p_streams(ctx);
+    if (st != MOE_OK) return bail(st);
+    cudaIpcMemHandle_t h[4];
+    if (cudaIpcGetMemHandle(&h[0], ctx->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->ybuf) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess || cudaIpcGetMemHandle(&h[3], ctx->retbuf) != cudaSuccess) {
+      fail(ctx, MOE_ERR_CUDA, "cudaIpcGetMemHandle failed");
       return bail(MOE_ERR_CUDA);
     }
+    const size_t hb = sizeof(h);
+    uint8_t* dh = nullptr;
+    std::vector<uint8_t> all(hb * G);
+    if (cudaMalloc(&dh, hb * (G + 1)) != cudaSuccess ||
+        cudaMemcpy(dh + hb * G, h, hb, cudaMemcpyHostToDevice) != cudaSuccess ||
+        ncclAllGather(dh + hb * G, dh, hb, ncclUint8, ctx->comm, 0) != ncclSuccess ||
+        cudaStreamSynchronize(0) != cudaSuccess || cudaMemcpy(all.data(), dh, hb * G, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      if (dh) cudaFree(dh);
+      fail(ctx, MOE_ERR_NCCL, "IPC handle exchange failed");
+      return bail(MOE_ERR_NCCL);
+    }
+    cudaFree(dh);
+    for (int g = 0; g < G; ++g) {
+      if (g == c.rank) {
+        dst[g] = ctx->recv;
+        src[g] = ctx->ybuf;
+        sig[g] = ctx->sig;
+        ret[g] = ctx->retbuf + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
+        continue;
+      }
+      const cudaIpcMemHandle_t* hg = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * g);
+      void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+      for (int i = 0; i < 4; ++i) {
+        cudaError_t e = cudaIpcOpenMemHandle(&p[i], hg[i], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          fail(ctx, MOE_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", g, cudaGetErrorString(e));
+          return bail(MOE_ERR_CUDA);
+        }
+        ctx->ipc_opened.push_back(p[i]);
+      }
+      dst[g] = p[0];
+      src[g] = p[1];
+      sig[g] = p[2];
+      // fused combine of TP slice tpi lands in partial region tpi of the source's buffer
+      ret[g] = static_cast<uint16_t*>(p[3]) + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
+    }
   }
-  if (cudaDeviceSynchronize() != cudaSuccess) {
-    fail(ctx, MOE_ERR_CUDA, "device sync after create failed");
-    return bail(MOE_ERR_CUDA);
-  }
+  st = upload_tables(ctx, dst, src, sig, ret);
+  if (st != MOE_OK) return bail(st);
   *out = ctx;
+  return MOE_OK;
+}
+
+moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t* devices, moe_ctx_t* out) {
+  moe_ctx_t ctx = nullptr;
+  if (!cfg || !out) return fail(ctx, MOE_ERR_INVALID_ARG, "cfg/out is NULL");
+  if (n < 2 || n > kMaxWorld) return fail(ctx, MOE_ERR_INVALID_ARG, "n=%d outside [2, %d]", n, kMaxWorld);
+  if (cfg->a2a_mode != MOE_A2A_P2P) return fail(ctx, MOE_ERR_UNSUPPORTED, "a single-process group needs MOE_A2A_P2P");
+  if (cfg->virtual_ranks > 1) return fail(ctx, MOE_ERR_INVALID_ARG, "a single-process group has no virtual ranks");
+  std::vector<moe_config> cf(n, *cfg);
+  for (int r = 0; r < n; ++r) {
+    cf[r].world = n;
+    cf[r].rank = r;
+    if (devices) cf[r].device = devices[r];
+    moe_status st = check_cfg(cf[r]);
+    if (st != MOE_OK) return st;
+  }
+  std::vector<moe_ctx_t> cs(n, nullptr);
+  auto bail = [&](moe_status s, moe_ctx_t culprit) {
+    std::string m = culprit ? culprit->err : g_err;
+    for (auto& c : cs) {
+      if (c) c->local_group = false;  // plain teardown (no peer devices to drain)
+      moe_ctx_destroy(c);
+    }
+    fail(nullptr, s, "%s", m.c_str());
+    return s;
+  };
+  auto devs = std::make_shared<std::vector<int>>();
+  for (int r = 0; r < n; ++r)
+    if (std::find(devs->begin(), devs->end(), cf[r].device) == devs->end()) devs->push_back(cf[r].device);
+  for (int r = 0; r < n; ++r) {
+    int share = 0;
+    for (int q = 0; q < n; ++q) share += cf[q].device == cf[r].device;
+    moe_status st = ctx_alloc(cf[r], share, &cs[r]);
+    if (st != MOE_OK) return bail(st, cs[r]);
+    cs[r]->local_group = true;
+    cs[r]->group_devices = devs;
+    st = p2p_streams(cs[r]);
+    if (st != MOE_OK) return bail(st, cs[r]);
+  }
+  // ranks on different devices of this process reach each other's memory as peers
+  for (int a : *devs)
+    for (int b : *devs) {
+      if (a == b) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a, b);
+      if (!can) {
+        fail(cs[0], MOE_ERR_UNSUPPORTED, "device %d cannot access device %d as a peer", a, b);
+        return bail(MOE_ERR_UNSUPPORTED, cs[0]);
+      }
+      cudaSetDevice(a);
+      cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        fail(cs[0], MOE_ERR_CUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", a, b, cudaGetErrorString(e));
+        return bail(MOE_ERR_CUDA, cs[0]);
+      }
+      cudaGetLastError();
+    }
+  for (int r = 0; r < n; ++r) {
+    moe_ctx_t c = cs[r];
+    std::vector<void*> dst(n), src(n), sig(n), ret(n);
+    for (int g = 0; g < n; ++g) {
+      dst[g] = cs[g]->recv;
+      src[g] = cs[g]->ybuf;
+      sig[g] = cs[g]->sig;
+      ret[g] = cs[g]->retbuf + (size_t)c->tpi * cs[g]->send_rows * c->H;
+    }
+    moe_status st = upload_tables(c, dst, src, sig, ret);
+    if (st != MOE_OK) return bail(st, c);
+  }
+  for (int r = 0; r < n; ++r) out[r] = cs[r];
   return MOE_OK;
 }
 
 moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   if (!ctx) return MOE_OK;
+  if (ctx->comm && ctx->cfg.world > 1) {
+    // collective: no peer may still read this rank's mapped buffers (a slower peer's
+    // combine pulling rows from ybuf) when they are freed -- barrier first
+    cudaSetDevice(ctx->cfg.device);
+    int* one = nullptr;
+    if (cudaMalloc(&one, sizeof(int)) == cudaSuccess) {
+      if (ncclAllReduce(one, one, 1, ncclInt32, ncclSum, ctx->comm, 0) == ncclSuccess) cudaStreamSynchronize(0);
+      cudaFree(one);
+    }
+  }
+  if (ctx->local_group && ctx->group_devices) {
+    // single-process group: the peers' kernels run on this process's devices
+    for (int d : *ctx->group_devices) {
+      cudaSetDevice(d);
+      cudaDeviceSynchronize();
+    }
+  }
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
   if (ctx->comm) {
@@ -576,21 +682,19 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_fork_cap) cudaEventDestroy(ctx->ev_fork_cap);
   if (ctx->ev_join_cap) cudaEventDestroy(ctx->ev_join_cap);
-  void* dev[] = {ctx->P_dev, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all, ctx->base_row,
-                 ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf, ctx->sendbuf,
-                 ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig, ctx->sig,
-                 ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
-                 ctx->item_of_slot, ctx->done_rows, ctx->push_work, ctx->epoch_dev, ctx->splitk_ws};
+  void* dev[] = {ctx->P_dev, ctx->P_all, ctx->tile_hist, ctx->tile_base, ctx->cnt_local, ctx->cnt_all,
+                 ctx->base_row, ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf,
+                 ctx->sendbuf, ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig,
+                 ctx->sig, ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
+                 ctx->epoch_dev, ctx->splitk_ws};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->tl)
     if (e) cudaEventDestroy(e);
-  if (ctx->P_pinned) cudaFreeHost(ctx->P_pinned);
+  if (ctx->P_all_pinned) cudaFreeHost(ctx->P_all_pinned);
   if (ctx->cnt_pinned) cudaFreeHost(ctx->cnt_pinned);
-  if (ctx->phash_pinned) cudaFreeHost(ctx->phash_pinned);
-  if (ctx->phash_dev) cudaFree(ctx->phash_dev);
   delete ctx;
   return MOE_OK;
 }
@@ -600,12 +704,14 @@ static moe_status check_device_error(moe_ctx_t ctx) {
   CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   if (e) {
     cudaMemset(ctx->err_dev, 0, sizeof(int));
-    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s%s",
+    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s%s%s%s",
                 (e & kErrBadExpert) ? " expert id out of range" : "",
                 (e & kErrCapacity) ? " receive capacity exceeded" : "",
                 (e & kErrTimeout) ? " P2P peer flag timeout (a rank skipped a collective call?)" : "",
                 (e & kErrPlacement) ? " ranks dispatched with different expert_to_rank maps" : "",
-                (e & kErrNaN) ? " NaN router logit" : "");
+                (e & kErrNaN) ? " NaN router logit" : "",
+                (e & kErrBadRank) ? " expert_to_rank value outside [0, G/tp)" : "",
+                (e & kErrWeights) ? " moe_expert_ffn n_w differs from the experts the placement hosts here" : "");
   }
   return MOE_OK;
 }
@@ -653,6 +759,7 @@ moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int
   if (E != ctx->E || !load) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
+  if (ctx->local_group) return fail(ctx, MOE_ERR_UNSUPPORTED, "statistics all-reduce in a single-process group");
   if (!ctx->comm) return MOE_OK;
   NC(ncclGroupStart());
   NC(ncclAllReduce(load, load, E, ncclInt64, ncclSum, ctx->comm, s));
@@ -667,6 +774,7 @@ moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coa
   if (E != ctx->E || !load || L < 1) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
+  if (ctx->local_group) return fail(ctx, MOE_ERR_UNSUPPORTED, "statistics all-reduce in a single-process group");
   if (!ctx->comm) return MOE_OK;
   NC(ncclGroupStart());
   NC(ncclAllReduce(load, load, (size_t)L * E, ncclInt64, ncclSum, ctx->comm, s));
@@ -696,22 +804,9 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   if (T > 0 && (!x || !idx)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
   const int E = ctx->E, G = ctx->G, H = ctx->H;
   const int n_grp = G / ctx->tp;  // EP ranks (groups of tp ranks when tp > 1)
-  for (int e = 0; e < E; ++e)
-    if (expert_to_rank[e] < 0 || expert_to_rank[e] >= n_grp)
-      return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank[%d]=%d outside [0, %d)", e, expert_to_rank[e], n_grp);
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   CU(cudaSetDevice(ctx->cfg.device));
-  if (!ctx->P_valid || memcmp(ctx->P_host.data(), expert_to_rank, sizeof(int32_t) * E) != 0) {
-    CU(cudaStreamSynchronize(s));  // the pinned staging copy may still be in flight
-    memcpy(ctx->P_pinned, expert_to_rank, sizeof(int32_t) * E);
-    memcpy(ctx->P_host.data(), expert_to_rank, sizeof(int32_t) * E);
-    CU(cudaMemcpyAsync(ctx->P_dev, ctx->P_pinned, sizeof(int32_t) * E, cudaMemcpyHostToDevice, s));
-    ctx->P_valid = true;
-  }
-  int n_hosted = 0;
-  for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || expert_to_rank[e] == ctx->grp);
-  ctx->n_hosted = n_hosted;
 
   ctx->tl_cur = ctx->tl_used < (int)ctx->tl_mask.size() ? ctx->tl_used : -1;
   if (ctx->tl_cur >= 0) ctx->tl_mask[ctx->tl_cur] = 0;
@@ -735,58 +830,48 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   }
   PlanArgs a = plan_args(ctx, T, k);
   PlanBuffers b = plan_buffers(ctx);
+  b.P_in = expert_to_rank;
   launch_count(a, idx, b, s);
   launch_scan(a, b, s);
   LAUNCHED(ctx, (a.n_tiles > 0) + 1);
   const bool nccl = ctx->comm != nullptr && !ctx->p2p;
   if (nccl) {
-    // the counts and a hash of the placement: all ranks must dispatch with the same map
-    uint32_t h = 2166136261u;
-    for (int e = 0; e < E; ++e) h = (h ^ (uint32_t)expert_to_rank[e]) * 16777619u;
-    ctx->phash_pinned[G] = h;
-    CU(cudaMemcpyAsync(ctx->phash_dev + G, ctx->phash_pinned + G, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    // the counts and every rank's placement: one all-gather, one host read (the
+    // send/recv segments are posted from the host); all ranks must dispatch with
+    // the same map (the call discipline of moe_dispatch)
     NC(ncclGroupStart());
     NC(ncclAllGather(ctx->cnt_local, ctx->cnt_all, E, ncclInt32, ctx->comm, s));
-    NC(ncclAllGather(ctx->phash_dev + G, ctx->phash_dev, 1, ncclUint32, ctx->comm, s));
+    NC(ncclAllGather(expert_to_rank, ctx->P_all, E, ncclInt32, ctx->comm, s));
     NC(ncclGroupEnd());
     CU(cudaMemcpyAsync(ctx->cnt_pinned, ctx->cnt_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost, s));
-    CU(cudaMemcpyAsync(ctx->phash_pinned, ctx->phash_dev, sizeof(uint32_t) * G, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ctx->P_all_pinned, ctx->P_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
     memcpy(ctx->cnt_host.data(), ctx->cnt_pinned, sizeof(int32_t) * G * E);
+    memcpy(ctx->P_host.data(), ctx->P_all_pinned + (size_t)ctx->me * E, sizeof(int32_t) * E);
+    for (int e = 0; e < E; ++e)
+      if (ctx->P_host[e] < 0 || ctx->P_host[e] >= n_grp) {
+        ctx->have_plan = false;
+        return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank[%d]=%d outside [0, %d)", e, ctx->P_host[e], n_grp);
+      }
     for (int g = 0; g < G; ++g)
-      if (ctx->phash_pinned[g] != h) {
+      if (memcmp(ctx->P_all_pinned + (size_t)g * E, ctx->P_host.data(), sizeof(int32_t) * E) != 0) {
         ctx->have_plan = false;
         return fail(ctx, MOE_ERR_DEVICE, "ranks dispatched with different expert_to_rank maps (rank %d differs)", g);
       }
   }
-  launch_layout(a, b, ctx->cap_rows, s);  // P2P: also the in-kernel count all-gather
+  launch_layout(a, b, ctx->cap_rows, s);  // validates P; P2P: also the in-kernel count all-gather
   tl_rec(ctx, 1, s);
   if (ctx->p2p) {
     // rows for peers: NVLink stores on the side stream (arrival flags raised by its
     // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
-    if (ctx->push_slot) {
-      // plan arrays (+ the send-order inverse) first; then the peers' rows leave in
-      // send order on the side stream, expert by expert with per-expert arrival
-      // flags, while this rank's own rows are copied on `stream` and K5 starts
-      launch_scatter(a, x, idx, b, 3, s);
-      CU(cudaEventRecord(ev_fork, s));
-      CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-      launch_push(a, x, b, ctx->num_sms, ctx->side);
-      tl_rec(ctx, 3, ctx->side);
-      CU(cudaEventRecord(ev_join, ctx->side));
-      launch_scatter(a, x, idx, b, 4, s);
-      tl_rec(ctx, 2, s);
-      LAUNCHED(ctx, 4);
-    } else {
-      CU(cudaEventRecord(ev_fork, s));
-      CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-      launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
-      tl_rec(ctx, 3, ctx->side);
-      CU(cudaEventRecord(ev_join, ctx->side));
-      launch_scatter(a, x, idx, b, 1, s);
-      tl_rec(ctx, 2, s);
-      LAUNCHED(ctx, 3);
-    }
+    CU(cudaEventRecord(ev_fork, s));
+    CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
+    launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
+    tl_rec(ctx, 3, ctx->side);
+    CU(cudaEventRecord(ev_join, ctx->side));
+    launch_scatter(a, x, idx, b, 1, s);
+    tl_rec(ctx, 2, s);
+    LAUNCHED(ctx, 3);
   } else {
     launch_scatter(a, x, idx, b, 0, s);
     tl_rec(ctx, 2, s);
@@ -828,16 +913,19 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   if (info) {
     memset(info, 0, sizeof *info);
     CU(cudaStreamSynchronize(s));
-    std::vector<int32_t> cnt((size_t)G * E);
+    std::vector<int32_t> cnt((size_t)G * E), P(E);
     CU(cudaMemcpy(cnt.data(), b.cnt_all, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(P.data(), ctx->P_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost));
     info->world = G;
+    int n_hosted = 0;
+    for (int e = 0; e < E; ++e) n_hosted += (ctx->virt || P[e] == ctx->grp);
     info->num_local_experts = n_hosted;
     int64_t rr = 0;
     for (int g = 0; g < n_grp && g < 64; ++g) {
       int64_t r = 0;
       for (int src = 0; src < G; ++src)
         for (int e = 0; e < E; ++e)
-          if (expert_to_rank[e] == g) r += cnt[src * E + e];
+          if (P[e] == g) r += cnt[src * E + e];
       info->recv_counts[g] = (int32_t)r;
       if (ctx->virt || g == ctx->grp) rr += r;
     }
@@ -845,7 +933,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
       for (int g = 0; g < n_grp && g < 64; ++g) {
         int64_t sc = 0;
         for (int e = 0; e < E; ++e)
-          if (expert_to_rank[e] == g) sc += cnt[ctx->me * E + e];
+          if (P[e] == g) sc += cnt[ctx->me * E + e];
         info->send_counts[g] = (int32_t)sc;
       }
     info->recv_rows = rr;
@@ -853,12 +941,15 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   return MOE_OK;
 }
 
-moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2, moe_stream_t stream) {
+moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2, int32_t n_w, moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
   if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_expert_ffn before moe_dispatch");
+  if (n_w < 0 || n_w > ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "n_w=%d outside [0, E]", n_w);
+  if (ctx->virt && n_w != ctx->E)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "virtual ranks host every expert: n_w=%d != E=%d", n_w, ctx->E);
+  if (n_w > 0 && (!w13 || !w2)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL weights");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
-  const int nw = ctx->n_hosted;
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
   // Fused combine (K6 returns rows over NVLink, staged in smem, one bulk copy per
@@ -871,29 +962,31 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     if (const char* env = getenv("MOE_FUSED_COMBINE")) fused = atoi(env) != 0;
     ctx->ffn_fused = ctx->p2p && fused;
   }
-  if (nw == 0) {
-    if (ctx->p2p) {  // no expert here: still tell every rank "my outputs are ready"
+  if (n_w == 0) {
+    // no expert here: the placement must host none on this rank (checked on the
+    // device), and in P2P mode every rank still hears "my outputs are ready"
+    launch_expect_nseg(ctx->seg_meta, 0, ctx->err_dev, s);
+    LAUNCHED(ctx, 1);
+    if (ctx->p2p) {
       launch_signal(a, b, 2, s);
       LAUNCHED(ctx, 1);
     }
     return MOE_OK;
   }
-  if (!w13 || !w2) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL weights");
   const int H = ctx->H, F = ctx->Fl, tp = ctx->tp;
   const bool vslices = ctx->virt && tp > 1;  // virtual TP: K6 once per FFN slice
-  const int nw_rows = ctx->virt ? ctx->E : nw;
-  if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != nw_rows) {
+  if (w13 != ctx->tmB1_ptr || w2 != ctx->tmB2_ptr || ctx->tmB_nw != n_w) {
     const int bn1 = gemm_b_box_rows(2 * F, true, ctx->gemm_cg), bn2 = gemm_b_box_rows(H, false, ctx->gemm_cg);
-    if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)nw_rows * 2 * F, H, bn1) ||
-        !make_tmap_2d(ctx->tmB2, w2, (uint64_t)nw_rows * H, F, bn2))
+    if (!make_tmap_2d(ctx->tmB1, w13, (uint64_t)n_w * 2 * F, H, bn1) ||
+        !make_tmap_2d(ctx->tmB2, w2, (uint64_t)n_w * H, F, bn2))
       return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for the weights");
     if (vslices)
       for (int q = 0; q < tp; ++q)
-        if (!make_tmap_2d_ld(ctx->tmB2s[q], w2 + (size_t)q * (F / tp), (uint64_t)nw_rows * H, F / tp, F, bn2))
+        if (!make_tmap_2d_ld(ctx->tmB2s[q], w2 + (size_t)q * (F / tp), (uint64_t)n_w * H, F / tp, F, bn2))
           return fail(ctx, MOE_ERR_CUDA, "cuTensorMapEncodeTiled failed for a W2 slice");
     ctx->tmB1_ptr = w13;
     ctx->tmB2_ptr = w2;
-    ctx->tmB_nw = nw_rows;
+    ctx->tmB_nw = n_w;
   }
   tl_rec(ctx, 4, s);
   const bool rec = ctx->timing_used < (int)ctx->ev.size() / 3;
@@ -901,43 +994,38 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (rec) CU(cudaEventRecord(ev[0], s));
   // P2P: K5's producer waits per tile for the source ranks whose rows the tile reads;
   // the tiles of this rank's own rows go first (overlapping the peers' NVLink pushes)
-  const SrcWait wait1{ctx->p2p ? (ctx->push_slot ? &ctx->sig->flag_seg[0][0] : ctx->sig->flag_data) : nullptr,
-                      ctx->seg_src, ctx->G, ctx->me, ctx->epoch_dev, ctx->push_slot ? 1 : 0};
-  const SrcWait nowait{nullptr, nullptr, 0, 0, 0, 0};
+  const SrcWait wait1{ctx->p2p ? ctx->sig->flag_data : nullptr, ctx->seg_src, ctx->G, ctx->me, ctx->epoch_dev};
+  const SrcWait nowait{nullptr, nullptr, 0, 0, nullptr};
   const FusedRet plain{nullptr, nullptr, 0, 0};
   // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
   // source rank's return buffer at the item's send-order slot -- the combine
   // all-to-all overlaps the expert GEMM tile by tile
   const FusedRet fused{ctx->ret_table, ctx->seg_src, ctx->G, ctx->ffn_fused ? 1 : 0};
-  // Split-K in decode-sized contexts (about one 128-row M tile per hosted expert):
-  // when a GEMM's output tiles cannot cover the SMs, split K into S slices (fp32
-  // partials in a workspace, ordered reduction -- deterministic).  Measured (graph
-  // replays, Mixtral layer, profiles/r1_v15_small_t_splitk_*): K6 at 4 GPUs (32
-  // tiles) 64 tokens 0.273 -> 0.252 ms, 256 tokens 0.293 -> 0.283 ms; no gain at 2
-  // GPUs (64 tiles) and a loss at 1 GPU (128 tiles: the partials' extra traffic), so
-  // only grids below a quarter of the SMs are split.
-  int ksplit = 1, ksplit5 = 1;
-  if (ctx->gemm_cg == 1 && !vslices) {
-    if (!ctx->ffn_fused) {
-      const long long tiles = (long long)nw * (H / gemm_block_n(H, false));
-      const int nkb = F / 64;
-      if (tiles * 4 < ctx->num_sms)
-        while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
-      if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
-    }
-    // K5 split-K is available (MOE_DECODE_SPLITK5=S) but off: measured slower at
-    // 2 and 4 GPUs (4 GPUs 64 tokens 0.246 -> 0.264 ms, profiles/r1_v15_small_t_k5split_*)
-    if (const char* env = getenv("MOE_DECODE_SPLITK5")) ksplit5 = std::max(1, atoi(env));
+  // Split-K of the down projection in decode-sized contexts (about one 128-row M tile
+  // per hosted expert): when K6's output tiles cannot cover the SMs, split K into S
+  // slices (fp32 partials in a workspace, ordered reduction -- deterministic).
+  // Measured (graph replays, Mixtral layer, profiles/r1_v15_small_t_splitk_*): K6 at
+  // 4 GPUs (32 tiles) 64 tokens 0.273 -> 0.252 ms, 256 tokens 0.293 -> 0.283 ms; no
+  // gain at 2 GPUs (64 tiles) and a loss at 1 GPU (128 tiles: the partials' extra
+  // traffic), so only grids below a quarter of the SMs are split.  (Splitting K5 the
+  // same way measured slower -- round 1 -- and was removed.)
+  int ksplit = 1;
+  if (ctx->gemm_cg == 1 && !vslices && !ctx->ffn_fused) {
+    const long long tiles = (long long)n_w * (H / gemm_block_n(H, false));
+    const int nkb = F / 64;
+    if (tiles * 4 < ctx->num_sms)
+      while (tiles * ksplit < ctx->num_sms && ksplit < 8 && nkb / (2 * ksplit) >= 4) ksplit *= 2;
+    if (const char* env = getenv("MOE_DECODE_SPLITK")) ksplit = std::max(1, atoi(env));
   }
-  if (ksplit > 1 || ksplit5 > 1) {
-    const size_t need = std::max((size_t)ksplit * ctx->cap_rows * H, (size_t)ksplit5 * ctx->cap_rows * 2 * F) *
-                        sizeof(float);
+  if (ksplit > 1) {
+    const size_t need = (size_t)ksplit * ctx->cap_rows * H * sizeof(float);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CU(cudaStreamIsCapturing(s, &cs));
-    if (need > ctx->splitk_bytes && cs != cudaStreamCaptureStatusNone) {
-      // no allocation inside a CUDA-graph capture: run this launch unsplit (an eager
-      // call before the capture sizes the workspace)
-      ksplit = ksplit5 = 1;
+    if (need > ctx->splitk_bytes && (cs != cudaStreamCaptureStatusNone || ctx->shared_dev)) {
+      // no allocation inside a CUDA-graph capture (an eager call before the capture
+      // sizes the workspace), nor next to a peer rank's kernels on this device (a
+      // cudaFree would wait for them): run this launch unsplit
+      ksplit = 1;
     } else if (need > ctx->splitk_bytes) {
       if (ctx->splitk_ws) CU(cudaFree(ctx->splitk_ws));
       ctx->splitk_ws = nullptr;
@@ -946,23 +1034,16 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
       ctx->splitk_bytes = need;
     }
   }
-  const long long pstride5 = (long long)ctx->cap_rows * 2 * F;
-  cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, 2 * F, H, true,
+  cudaError_t e = launch_grouped_gemm(ctx->tmA1, ctx->tmB1, ctx->hbuf, F, ctx->seg_meta, ctx->E, n_w, 2 * F, H, true,
                                       ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
-                                      s, ksplit5, ctx->splitk_ws, pstride5, ctx->tmDh);
+                                      s, 1, nullptr, 0, ctx->tmDh);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
-  if (ksplit5 > 1) {
-    e = launch_splitk_reduce_swiglu(ctx->splitk_ws, pstride5, ksplit5, ctx->seg_meta, ctx->E, F, ctx->gemm_cg,
-                                    ctx->hbuf, F, ctx->num_sms, s);
-    if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "split-K SwiGLU reduce launch: %s", cudaGetErrorString(e));
-    ctx->launches += 1;
-  }
   if (rec) CU(cudaEventRecord(ev[1], s));
   tl_rec(ctx, 5, s);
   if (!vslices) {
     const long long pstride = (long long)ctx->cap_rows * H;
-    e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, H, F, false, ctx->gemm_cg,
-                            ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s, ksplit,
+    e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, n_w, H, F, false,
+                            ctx->gemm_cg, ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s, ksplit,
                             ctx->splitk_ws, pstride, ctx->tmDy);
     if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 launch: %s", cudaGetErrorString(e));
     if (ksplit > 1) {
@@ -976,7 +1057,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     // into expert-output buffer q; the combine sums the slices
     for (int q = 0; q < tp; ++q) {
       e = launch_grouped_gemm(ctx->tmA2s[q], ctx->tmB2s[q], ctx->ybuf + (size_t)q * ctx->cap_rows * H, H,
-                              ctx->seg_meta, ctx->E, H, F / tp, false, ctx->gemm_cg, ctx->num_sms, nowait,
+                              ctx->seg_meta, ctx->E, n_w, H, F / tp, false, ctx->gemm_cg, ctx->num_sms, nowait,
                               ctx->err_dev, ctx->done_counter + 2, plain, s, 1, nullptr, 0, ctx->tmDys[q]);
       if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm2 slice launch: %s", cudaGetErrorString(e));
     }
@@ -1110,6 +1191,16 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   }
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
+  if (ctx->p2p && (a.n_tiles == 0 || ctx->shared_dev)) {
+    // every rank's expert outputs of this layer are ready (flag_y).  A rank without
+    // tokens must wait too: its next dispatch writes count rows into the peers'
+    // signal blocks, which they read until their own layout kernel of this layer is
+    // done -- and every peer raises flag_y only after that.  Ranks sharing a device
+    // wait with one CTA here instead of with every CTA of the combine (those would
+    // hold the SMs a peer's expert GEMM needs to raise the flag).
+    launch_wait(ctx->sig->flag_y, ctx->G, ctx->epoch_dev, ctx->err_dev, s);
+    LAUNCHED(ctx, 1);
+  }
   launch_combine(a, w, b, out, s);
   LAUNCHED(ctx, a.n_tiles > 0);
   tl_rec(ctx, 7, s);
@@ -1130,7 +1221,8 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
   moe_status st = check_device_error(ctx);
   if (st != MOE_OK) return st;
   const int E = ctx->E, G = ctx->G, T = ctx->last_T, k = ctx->last_k;
-  std::vector<int32_t> cnt((size_t)G * E), rows((size_t)std::max(1, T * k));
+  std::vector<int32_t> cnt((size_t)G * E), rows((size_t)std::max(1, T * k)), Pv(E);
+  CU(cudaMemcpy(Pv.data(), ctx->P_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost));
   std::vector<uint8_t> slots((size_t)std::max(1, T * k));
   const int32_t* cnt_dev = plan_buffers(ctx).cnt_all;
   CU(cudaMemcpy(cnt.data(), cnt_dev, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost));
@@ -1140,9 +1232,9 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
   }
   // P2P: per-rank padded layout of the destination rank
   std::vector<int32_t> peer_base((size_t)G * E);
-  layout_host_impl(E, G, ctx->P_host.data(), cnt.data(), ctx->seg_align, nullptr, peer_base.data(), nullptr, nullptr);
+  layout_host_impl(E, G, Pv.data(), cnt.data(), ctx->seg_align, nullptr, peer_base.data(), nullptr, nullptr);
   if (cnt_out) memcpy(cnt_out, cnt.data(), sizeof(int32_t) * G * E);
-  const int32_t* P = ctx->P_host.data();
+  const int32_t* P = Pv.data();
   // unpadded receive start of (e, s) on rank P[e]; send-order base of (s, e)
   std::vector<int64_t> ustart((size_t)G * E), sbase((size_t)G * E), cbase(E);
   for (int g = 0; g < G; ++g) {

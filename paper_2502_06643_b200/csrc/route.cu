@@ -163,4 +163,12 @@ void launch_route_stats(const int32_t* idx_l, const int32_t* idx_l1, int T, int 
                                               (unsigned long long*)coact, err, smem_co);
 }
 
+void preload_route_kernels() {
+  cudaFuncAttributes fa;
+  const void* fs[] = {(const void*)k_route<4, 1>, (const void*)k_route<8, 1>, (const void*)k_route<16, 1>,
+                      (const void*)k_route<32, 1>, (const void*)k_route<32, 2>, (const void*)k_route<32, 4>,
+                      (const void*)k_route<32, 8>, (const void*)k_route_stats};
+  for (const void* f : fs) cudaFuncGetAttributes(&fa, f);
+}
+
 }  // namespace moe

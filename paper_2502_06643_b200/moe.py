@@ -16,12 +16,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmoe.so")
 
 MOE_OK = 0
-ABI_VERSION = 2  # include/moe.h MOE_ABI_VERSION (moe_config layout)
+ABI_VERSION = 3  # include/moe.h MOE_ABI_VERSION
 STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_CUDA", 3: "MOE_ERR_NCCL", 4: "MOE_ERR_CAPACITY",
           5: "MOE_ERR_UNSUPPORTED", 6: "MOE_ERR_DEVICE", 7: "MOE_ERR_TIMEOUT"}
 
 # Every symbol include/moe.h declares (checked by tests/test_abi_cpu.py).
-EXPORTS = ["moe_get_unique_id", "moe_ctx_create", "moe_ctx_destroy", "moe_ctx_sync", "moe_status_str",
+EXPORTS = ["moe_get_unique_id", "moe_ctx_create", "moe_ctx_create_group", "moe_ctx_destroy", "moe_ctx_sync", "moe_status_str",
            "moe_last_error", "moe_abi_version", "moe_route", "moe_route_stats", "moe_stats_allreduce", "moe_stats_allreduce_layers",
            "moe_dispatch", "moe_expert_ffn", "moe_combine", "moe_pack_w13", "moe_placement_contiguous",
            "moe_layout_host", "moe_debug_plan", "moe_debug_identity_ffn", "moe_debug_recv", "moe_kernel_launches",
@@ -55,6 +55,7 @@ def load_library(path=LIB_PATH):
     sig = {
         "moe_get_unique_id": [P],
         "moe_ctx_create": [ctypes.POINTER(Config), P, ctypes.POINTER(P)],
+        "moe_ctx_create_group": [ctypes.POINTER(Config), I32, P, P],
         "moe_ctx_destroy": [P],
         "moe_ctx_sync": [P],
         "moe_route": [P, P, I32, I32, I32, P, P, P],
@@ -62,7 +63,7 @@ def load_library(path=LIB_PATH):
         "moe_stats_allreduce": [P, P, P, I32, P],
         "moe_stats_allreduce_layers": [P, P, P, I32, I32, P],
         "moe_dispatch": [P, P, P, I32, I32, P, P, P],
-        "moe_expert_ffn": [P, P, P, P],
+        "moe_expert_ffn": [P, P, P, I32, P],
         "moe_combine": [P, P, P, P],
         "moe_pack_w13": [P, P, I32, I32, I32, P, P],
         "moe_placement_contiguous": [I32, I32, P],
@@ -107,6 +108,24 @@ def _check(status, ctx=None):
 def _ptr(t):
     if t is None:
         return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _dev(t, dtype, device, name, ndim=None):
+    """Device pointer of a tensor argument after checking what the C ABI assumes
+    (dtype, dense row-major, on this context's device); None passes through."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise MoeError(1, f"{name}: expected a torch tensor, got {type(t).__name__}")
+    if t.dtype != dtype:
+        raise MoeError(1, f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise MoeError(1, f"{name}: must be contiguous")
+    if t.device != device:
+        raise MoeError(1, f"{name}: on {t.device}, the context is on {device}")
+    if ndim is not None and t.dim() != ndim:
+        raise MoeError(1, f"{name}: {t.dim()} dims, expected {ndim}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -167,24 +186,45 @@ class MoeLayer:
     """One libmoe context (one EP rank, or G virtual ranks on one GPU).
 
     tp > 1: tensor parallelism inside the experts (moe.h; reading G20) -- the G
-    ranks form G/tp EP groups, the placement maps experts to groups."""
+    ranks form G/tp EP groups, the placement maps experts to groups.
+    MoeLayer.group(n, ...): the n ranks of an EP group as n contexts of this
+    process (moe_ctx_create_group), e.g. all on one GPU."""
 
     def __init__(self, *, max_tokens, hidden, ffn, num_experts, max_k, world=1, rank=0, device=0,
-                 virtual_ranks=1, uid=None, a2a="nccl", tp=1):
+                 virtual_ranks=1, uid=None, a2a="nccl", tp=1, _handle=None):
         mode = {"nccl": 0, "p2p": 1}[a2a]
         self.cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, world, rank, device, virtual_ranks, mode, tp)
         self.a2a = a2a
         self.tp = tp
+        self.rank = rank
         self.E, self.H, self.F = num_experts, hidden, ffn
         self.G = virtual_ranks if virtual_ranks > 1 else world
         self.device = torch.device("cuda", device)
+        self._placements = {}
+        self._last = None
+        if _handle is not None:
+            self._ctx = _handle
+            return
         h = ctypes.c_void_p()
         uid_buf = None
         if uid is not None:
             uid_buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(_lib.moe_ctx_create(ctypes.byref(self.cfg), uid_buf, ctypes.byref(h)))
         self._ctx = h
-        self._last = None
+
+    @classmethod
+    def group(cls, n, *, max_tokens, hidden, ffn, num_experts, max_k, devices=None, tp=1):
+        """The n ranks of an EP group as n contexts of this process (moe.h,
+        moe_ctx_create_group; P2P data plane, peer pointers without IPC/NCCL).
+        devices: list of n device ordinals (default: all on the current device)."""
+        dev0 = torch.cuda.current_device() if devices is None else int(devices[0])
+        cfg = Config(max_tokens, hidden, ffn, num_experts, max_k, n, 0, dev0, 1, 1, tp)
+        hs = (ctypes.c_void_p * n)()
+        darr = None if devices is None else (ctypes.c_int32 * n)(*[int(d) for d in devices])
+        _check(_lib.moe_ctx_create_group(ctypes.byref(cfg), n, darr, hs))
+        return [cls(max_tokens=max_tokens, hidden=hidden, ffn=ffn, num_experts=num_experts, max_k=max_k, world=n,
+                    rank=r, device=dev0 if devices is None else int(devices[r]), a2a="p2p", tp=tp,
+                    _handle=ctypes.c_void_p(hs[r])) for r in range(n)]
 
     def close(self):
         if self._ctx:
@@ -242,36 +282,67 @@ class MoeLayer:
             idx = torch.empty(T, k, dtype=torch.int32, device=logits.device)
         if w is None:
             w = torch.empty(T, k, dtype=torch.float32, device=logits.device)
-        self._c(_lib.moe_route(self._ctx, _ptr(logits), T, E, k, _ptr(idx), _ptr(w), _stream(stream)))
+        d = self.device
+        self._c(_lib.moe_route(self._ctx, _dev(logits, torch.float32, d, "logits", 2), T, E, k,
+                               _dev(idx, torch.int32, d, "idx", 2), _dev(w, torch.float32, d, "w", 2),
+                               _stream(stream)))
         return idx, w
 
     # a2
     def route_stats(self, idx_l, idx_l1, load, coact, stream=None):
         T, k = idx_l.shape
-        self._c(_lib.moe_route_stats(self._ctx, _ptr(idx_l), _ptr(idx_l1), T, self.E, k, _ptr(load), _ptr(coact),
+        d = self.device
+        self._c(_lib.moe_route_stats(self._ctx, _dev(idx_l, torch.int32, d, "idx_l", 2),
+                                     _dev(idx_l1, torch.int32, d, "idx_l1", 2), T, self.E, k,
+                                     _dev(load, torch.int64, d, "load"), _dev(coact, torch.int64, d, "coact"),
                                      _stream(stream)))
 
     def stats_allreduce(self, load, coact, stream=None):
-        self._c(_lib.moe_stats_allreduce(self._ctx, _ptr(load), _ptr(coact), self.E, _stream(stream)))
+        d = self.device
+        self._c(_lib.moe_stats_allreduce(self._ctx, _dev(load, torch.int64, d, "load"),
+                                         _dev(coact, torch.int64, d, "coact"), self.E, _stream(stream)))
 
     def stats_allreduce_layers(self, load, coact, stream=None):
         """load int64 [L][E], coact int64 [L-1][E][E] (or None): one collective."""
         L = load.shape[0]
-        self._c(_lib.moe_stats_allreduce_layers(self._ctx, _ptr(load), _ptr(coact), self.E, L, _stream(stream)))
+        d = self.device
+        self._c(_lib.moe_stats_allreduce_layers(self._ctx, _dev(load, torch.int64, d, "load"),
+                                                _dev(coact, torch.int64, d, "coact"), self.E, L, _stream(stream)))
+
+    def placement(self, expert_to_rank):
+        """The device int32 [E] placement array moe_dispatch reads.  A torch tensor on
+        this device passes through; a host sequence is uploaded once and cached (by
+        value), so repeated dispatches with the same placement copy nothing."""
+        if isinstance(expert_to_rank, torch.Tensor) and expert_to_rank.is_cuda:
+            return expert_to_rank
+        P = np.ascontiguousarray(np.asarray(expert_to_rank), dtype=np.int32)
+        key = P.tobytes()
+        t = self._placements.get(key)
+        if t is None:
+            t = torch.from_numpy(P.copy()).to(self.device)
+            self._placements[key] = t
+        return t
 
     # a3-a5
     def dispatch(self, x, idx, expert_to_rank, info=False, stream=None):
         T, k = idx.shape
-        P = np.ascontiguousarray(expert_to_rank, dtype=np.int32)
+        d = self.device
+        P = self.placement(expert_to_rank)
         inf = DispatchInfo() if info else None
-        self._c(_lib.moe_dispatch(self._ctx, _ptr(x), _ptr(idx), T, k, _np_ptr(P),
+        self._c(_lib.moe_dispatch(self._ctx, _dev(x, torch.bfloat16, d, "x", 2), _dev(idx, torch.int32, d, "idx", 2),
+                                  T, k, _dev(P, torch.int32, d, "expert_to_rank", 1),
                                   ctypes.byref(inf) if inf is not None else None, _stream(stream)))
         self._last = (T, k)
         return inf
 
     # a6
     def expert_ffn(self, w13, w2, stream=None):
-        self._c(_lib.moe_expert_ffn(self._ctx, _ptr(w13), _ptr(w2), _stream(stream)))
+        """w13 bf16 [n_w][2F][H] (pack_w13), w2 bf16 [n_w][H][F]: the experts the last
+        dispatch's placement hosts here (n_w may be 0: w13 = w2 = None)."""
+        d = self.device
+        n_w = 0 if w13 is None else int(w13.shape[0])
+        self._c(_lib.moe_expert_ffn(self._ctx, _dev(w13, torch.bfloat16, d, "w13", 3),
+                                    _dev(w2, torch.bfloat16, d, "w2", 3), n_w, _stream(stream)))
 
     def identity_ffn(self, stream=None):
         self._c(_lib.moe_debug_identity_ffn(self._ctx, _stream(stream)))
@@ -281,7 +352,9 @@ class MoeLayer:
         T, k = self._last
         if out is None:
             out = torch.empty(T, self.H, dtype=torch.bfloat16, device=self.device)
-        self._c(_lib.moe_combine(self._ctx, _ptr(w), _ptr(out), _stream(stream)))
+        d = self.device
+        self._c(_lib.moe_combine(self._ctx, _dev(w, torch.float32, d, "w", 2), _dev(out, torch.bfloat16, d, "out", 2),
+                                 _stream(stream)))
         return out
 
     # debug views

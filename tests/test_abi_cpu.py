@@ -42,7 +42,7 @@ def test_every_declared_symbol_is_exported():
     for name in decl:
         assert hasattr(lib, name), name
     assert sorted(moe.EXPORTS) == decl
-    assert lib.moe_abi_version() == 2
+    assert lib.moe_abi_version() == 3
     assert lib.moe_status_str(4) == b"MOE_ERR_CAPACITY"
 
 
@@ -74,7 +74,26 @@ def test_null_ctx_calls_fail_cleanly():
     lib = moe.lib()
     assert lib.moe_route(None, None, 1, 8, 2, None, None, None) == 1
     assert lib.moe_dispatch(None, None, None, 1, 2, None, None, None) == 1
+    assert lib.moe_expert_ffn(None, None, None, 0, None) == 1
     assert lib.moe_combine(None, None, None, None) == 1
+
+
+def test_group_create_validates_before_touching_the_device():
+    """moe_ctx_create_group (single-process EP group): P2P only, n >= 2, no
+    virtual ranks, and every rank's config passes the moe_ctx_create checks."""
+    moe = _moe()
+    lib = moe.lib()
+    base = dict(max_tokens=16, hidden=64, ffn=128, num_experts=8, max_k=2, world=1, rank=0, device=0,
+                virtual_ranks=1, a2a_mode=1, tp=1)
+    bad = [(dict(), 1), (dict(a2a_mode=0), 4), (dict(virtual_ranks=4), 4), (dict(hidden=96), 4),
+           (dict(tp=3), 4), (dict(), 65)]
+    for upd, n in bad:
+        kw = dict(base)
+        kw.update(upd)
+        cfg = moe.Config(*[kw[f] for f, _ in moe.Config._fields_])
+        hs = (ctypes.c_void_p * max(n, 1))()
+        st = lib.moe_ctx_create_group(ctypes.byref(cfg), n, None, hs)
+        assert st in (1, 5), (upd, n, st)
 
 
 def _layout_checks(moe, P, cnt, idx_by_source):

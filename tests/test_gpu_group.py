@@ -1,0 +1,342 @@
+"""The real multi-rank data plane on ONE GPU: a single-process EP group
+(moe_ctx_create_group) of G rank contexts on cuda:0, each rank with its own
+streams, buffers and signal block, talking through the same P2P code as G
+processes on G GPUs -- the in-kernel count all-gather of k_layout, the
+side-stream scatter of the peers' rows, K5's per-tile arrival waits, the fused
+(K6 epilogue) and pulled (K8) combines, the TP all-gather fan-out and partial
+return -- with the peers' device pointers in the tables instead of CUDA IPC
+mappings (an IPC handle cannot be opened by the process that exported it).
+
+Checked against the oracle (the all-to-all before and after the expert FFN,
+P:L824; the expert -> GPU map): the plan (count matrix, send slots,
+receive positions, destinations) and the received payload bit-exactly, the
+identity-expert round trip bit-exactly, the layer output bit-identical to the
+virtual-rank run and within 2e-2 of the oracle (G16).  Ranks are issued from
+one host thread in rank order; no call blocks on a peer.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import layer as olayer
+from oracle import plan as oplan
+from oracle import route as oroute
+from tests._util import Inputs, assert_close_layer, bf16_to_f64
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0)
+
+
+def _moe():
+    from paper_2502_06643_b200 import moe
+    return moe
+
+
+class Group:
+    """G rank contexts of one EP group on cuda:0, one stream per rank."""
+
+    def __init__(self, G, T, H, F, E, k, tp=1):
+        moe = _moe()
+        self.G, self.tp = G, tp
+        self.blocks = oplan.token_blocks(T, G)
+        tmax = max(max(b - a for a, b in self.blocks), 1)
+        self.lays = moe.MoeLayer.group(G, max_tokens=tmax, hidden=H, ffn=F, num_experts=E, max_k=k, tp=tp)
+        self.streams = [torch.cuda.Stream(device=DEV) for _ in range(G)]
+
+    def each(self, fn):
+        """fn(r, layer) for every rank, issued on rank r's stream; returns the results."""
+        res = []
+        for r, lay in enumerate(self.lays):
+            with torch.cuda.stream(self.streams[r]):
+                res.append(fn(r, lay))
+        return res
+
+    def sync(self):
+        for lay in self.lays:
+            lay.sync()
+        torch.cuda.synchronize()
+
+    def close(self):
+        torch.cuda.synchronize()
+        for lay in self.lays:
+            lay.close()
+
+
+def _setup(inp, g, k):
+    x_all, logits_all = inp.to_device(DEV)
+    xs = [x_all[a:b].contiguous() for a, b in g.blocks]
+    ls = [logits_all[a:b].contiguous() for a, b in g.blocks]
+    torch.cuda.synchronize()
+    return x_all, logits_all, xs, ls
+
+
+def _virtual_out(inp, P, G, k, tp=1):
+    moe = _moe()
+    T, H, F, E = inp.T, inp.H, inp.F, inp.E
+    vl = moe.MoeLayer(max_tokens=T, hidden=H, ffn=F, num_experts=E, max_k=k, virtual_ranks=G, tp=tp)
+    x_all, logits_all = inp.to_device(DEV)
+    vi, vw = vl.route(logits_all, k)
+    vl.dispatch(x_all, vi, P)
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E)))
+    vl.expert_ffn(moe.pack_w13(w1, w3), w2)
+    out = vl.combine(vw)
+    vl.sync()
+    vl.close()
+    return out
+
+
+PLACEMENTS = {
+    2: [[0, 0, 0, 0, 1, 1, 1, 1], [0, 1, 1, 1, 0, 1, 0, 1], [1] * 6 + [0, 0]],
+    4: [[0, 0, 1, 1, 2, 2, 3, 3], [0, 1, 2, 2, 3, 2, 3, 3], [3] * 6 + [0, 0]],   # last: ranks 1, 2 host nothing
+}
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("G", [2, 4])
+def test_group_plan_payload_and_layer(cuda_ok, G, fused, monkeypatch):
+    monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
+    moe = _moe()
+    T, H, F, E, k = 1500, 256, 512, 8, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=21 + G)
+    g = Group(G, T, H, F, E, k)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    ridx, _ = oroute.route(inp.logits.numpy(), k)
+    ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+    for P in PLACEMENTS[G]:
+        P = np.array(P)
+        for lay in g.lays:
+            lay.placement(P)          # upload the device placement before any rank's layer is issued
+        torch.cuda.synchronize()
+        rw = g.each(lambda r, lay: lay.route(ls[r], k))
+        g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        pl = oplan.plan([ridx[a:b] for a, b in g.blocks], P, G)
+        for r, lay in enumerate(g.lays):
+            dr, rp, ss, cnt = lay.debug_plan()
+            a, b = g.blocks[r]
+            assert np.array_equal(cnt, pl["cnt"]), "count matrix (in-kernel all-gather)"
+            assert np.array_equal(ss, pl["slot"][r]), "send slots"
+            assert np.array_equal(rp, pl["recv_pos"][r]), "receive positions"
+            assert np.array_equal(dr, P[ridx[a:b]]), "destination ranks"
+            rows = lay.debug_recv()
+            ref_rows = xb[[g.blocks[s][0] + t for (s, t, j, e) in pl["recv"][r]]].reshape(-1, H)
+            assert np.array_equal(rows, ref_rows), f"received payload of rank {r}"
+        g.each(lambda r, lay: lay.identity_ffn())
+        outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+        g.sync()
+        for r in range(G):
+            assert torch.equal(outs[r].view(torch.int16), xs[r].view(torch.int16)), "identity round trip"
+        # the real expert FFN: K5 waits per tile for the peers' rows, K6 returns them
+        ws = []
+        for r in range(G):
+            hosted = [e for e in range(E) if P[e] == r]
+            if hosted:
+                w1, w3, w2 = inp.device_weights(DEV, hosted)
+                ws.append((moe.pack_w13(w1, w3), w2))
+            else:
+                ws.append((None, None))
+        torch.cuda.synchronize()
+        g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
+        outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+        g.sync()
+        out = torch.cat(outs)
+        virt = _virtual_out(inp, P, G, k)
+        assert torch.equal(out.view(torch.int16), virt.view(torch.int16)), "cross-mode equality (group vs virtual)"
+        assert_close_layer(bf16_to_f64(out), ref)
+    g.close()
+
+
+@pytest.mark.parametrize("G,tp,fused", [(2, 2, "0"), (2, 2, "1"), (4, 2, "1"), (4, 4, "0")])
+def test_group_tensor_parallel(cuda_ok, G, tp, fused, monkeypatch):
+    """EP x TP over G ranks of one GPU (reading G20): the TP all-gather fan-out of
+    the dispatch and the bf16 partial return of the combine, against the oracle's
+    TP layer and the virtual-rank TP run."""
+    monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
+    moe = _moe()
+    T, H, F, E, k = 1100, 256, 512, 8, 2
+    n_grp = G // tp
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=31 + G + tp)
+    g = Group(G, T, H, F, E, k, tp=tp)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    ridx, _ = oroute.route(inp.logits.numpy(), k)
+    w1a, w3a, w2a = inp.device_weights(DEV, list(range(E)))
+    xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+    for P in ([e * n_grp // E for e in range(E)], [0, 1, 1, 1, 0, 1, 0, 1]):
+        P = np.array(P) % n_grp
+        ws = []
+        for r in range(G):
+            hosted = [e for e in range(E) if P[e] == r // tp]
+            if hosted:
+                sel = torch.tensor(hosted, device=DEV)
+                ws.append(moe.tp_slice_weights(w1a[sel], w3a[sel], w2a[sel], tp, r % tp))
+            else:
+                ws.append((None, None))
+            g.lays[r].placement(P)
+        torch.cuda.synchronize()
+        rw = g.each(lambda r, lay: lay.route(ls[r], k))
+        g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        pl = oplan.plan([ridx[a:b] for a, b in g.blocks], P, n_grp)
+        for r, lay in enumerate(g.lays):
+            dr, rp, ss, cnt = lay.debug_plan()
+            assert np.array_equal(cnt, pl["cnt"])
+            assert np.array_equal(ss, pl["slot"][r])
+            assert np.array_equal(rp, pl["recv_pos"][r])
+            rows = lay.debug_recv()                      # every TP rank of a group holds its rows
+            ref_rows = xb[[g.blocks[s][0] + t for (s, t, j, e) in pl["recv"][r // tp]]].reshape(-1, H)
+            assert np.array_equal(rows, ref_rows)
+        g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
+        outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+        g.sync()
+        out = torch.cat(outs)
+        virt = _virtual_out(inp, P, G, k, tp=tp)
+        assert torch.equal(out.view(torch.int16), virt.view(torch.int16)), "cross-mode equality (TP)"
+        ref, _, _, _ = olayer.layer_ep_tp(bf16_to_f64(inp.x), inp.logits.numpy(), k, P, n_grp, tp,
+                                          inp.oracle_tp_fn(tp))
+        assert_close_layer(bf16_to_f64(out), ref)
+    g.close()
+
+
+def test_group_zero_token_ranks_and_per_layer_placements(cuda_ok):
+    """Ranks owning 0 tokens (G7) and a different device placement every layer:
+    the T = 0 rank's combine waits for every rank's expert outputs, so its next
+    dispatch cannot overwrite count rows a peer is still reading (8 layers,
+    epochs advance, the placement array changes between layers with no host
+    synchronisation)."""
+    moe = _moe()
+    G, H, F, E, k = 4, 128, 256, 8, 2
+    T = 3                                  # ranks 0..2 own 1 token, rank 3 none
+    inp = Inputs(64, H, F, E, k, s=1.6, seed=5)
+    g = Group(G, T, H, F, E, k)
+    x_all, logits_all = inp.to_device(DEV)
+    xs = [x_all[:T][a:b].contiguous() for a, b in g.blocks]
+    ls = [logits_all[:T][a:b].contiguous() for a, b in g.blocks]
+    plans = [np.array(p) for p in ([0, 0, 1, 1, 2, 2, 3, 3], [3, 2, 1, 0, 0, 1, 2, 3], [1] * 8,
+                                   [0, 1, 2, 2, 3, 2, 3, 3])]
+    w1a, w3a, w2a = inp.device_weights(DEV, list(range(E)))
+    wsets = []
+    for P in plans:
+        row = []
+        for r in range(G):
+            hosted = [e for e in range(E) if P[e] == r]
+            sel = torch.tensor(hosted, device=DEV, dtype=torch.long)
+            row.append((moe.pack_w13(w1a[sel], w3a[sel]), w2a[sel].contiguous()) if hosted else (None, None))
+            g.lays[r].placement(P)
+        wsets.append(row)
+    torch.cuda.synchronize()
+    outs_all = []
+    for layer in range(8):
+        li = layer % len(plans)
+        P = plans[li]
+        rw = g.each(lambda r, lay: lay.route(ls[r], k))
+        g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        g.each(lambda r, lay: lay.expert_ffn(*wsets[li][r]))
+        outs_all.append(g.each(lambda r, lay: lay.combine(rw[r][1])))
+    g.sync()
+    ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x[:T]), inp.logits[:T].numpy(), k, inp.oracle_expert_fn())
+    for outs in outs_all:
+        assert outs[3].shape == (0, H)
+        assert_close_layer(bf16_to_f64(torch.cat(outs)), ref)
+        assert torch.equal(torch.cat(outs).view(torch.int16), torch.cat(outs_all[0]).view(torch.int16))
+    g.close()
+
+
+def test_group_graph_capture_per_layer_placements(cuda_ok):
+    """Each rank's 4-layer chain -- a different device placement per layer --
+    captured into one CUDA graph per rank and replayed (device-side flag epoch,
+    device placement arrays: no host synchronisation inside the chain); replays
+    are bit-identical to the eager chain."""
+    moe = _moe()
+    G, T, H, F, E, k, L = 2, 600, 256, 512, 8, 2, 4
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=9)
+    g = Group(G, T, H, F, E, k)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    plans = [np.array(p) for p in ([0, 0, 0, 0, 1, 1, 1, 1], [0, 1, 1, 1, 0, 1, 0, 1], [1, 0, 1, 0, 1, 0, 1, 0],
+                                   [1, 1, 1, 1, 1, 1, 0, 0])]
+    w1a, w3a, w2a = inp.device_weights(DEV, list(range(E)))
+    wl, Pd = [], []
+    for r in range(G):
+        wl.append([])
+        Pd.append([])
+        for P in plans:
+            hosted = [e for e in range(E) if P[e] == r]
+            sel = torch.tensor(hosted, device=DEV, dtype=torch.long)
+            wl[r].append((moe.pack_w13(w1a[sel], w3a[sel]), w2a[sel].contiguous()) if hosted else (None, None))
+            Pd[r].append(g.lays[r].placement(P))
+    bufs = [[torch.empty_like(xs[r]) for _ in range(L)] for r in range(G)]
+    idx = [torch.empty(xs[r].shape[0], k, dtype=torch.int32, device=DEV) for r in range(G)]
+    wts = [torch.empty(xs[r].shape[0], k, dtype=torch.float32, device=DEV) for r in range(G)]
+    torch.cuda.synchronize()
+
+    def chain(r, lay):
+        xin = xs[r]
+        for li in range(L):
+            lay.route(ls[r], k, idx[r], wts[r])
+            lay.dispatch(xin, idx[r], Pd[r][li])
+            lay.expert_ffn(*wl[r][li])
+            lay.combine(wts[r], bufs[r][li])
+            xin = bufs[r][li]
+
+    # eager (layer by layer across ranks, as a real group would run)
+    def eager():
+        for li in range(L):
+            for r, lay in enumerate(g.lays):
+                with torch.cuda.stream(g.streams[r]):
+                    xin = xs[r] if li == 0 else bufs[r][li - 1]
+                    lay.route(ls[r], k, idx[r], wts[r])
+                    lay.dispatch(xin, idx[r], Pd[r][li])
+            for r, lay in enumerate(g.lays):
+                with torch.cuda.stream(g.streams[r]):
+                    lay.expert_ffn(*wl[r][li])
+            for r, lay in enumerate(g.lays):
+                with torch.cuda.stream(g.streams[r]):
+                    lay.combine(wts[r], bufs[r][li])
+        g.sync()
+
+    eager()
+    ref = [[b.clone() for b in bufs[r]] for r in range(G)]
+    graphs = []
+    for r, lay in enumerate(g.lays):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=g.streams[r]):
+            chain(r, lay)
+        graphs.append(gr)
+    for rep in range(3):
+        for r in range(G):
+            for b in bufs[r]:
+                b.zero_()
+        torch.cuda.synchronize()
+        for r in range(G):
+            with torch.cuda.stream(g.streams[r]):
+                graphs[r].replay()
+        g.sync()
+        for r in range(G):
+            for li in range(L):
+                assert torch.equal(bufs[r][li].view(torch.int16), ref[r][li].view(torch.int16)), (rep, r, li)
+    ref_l0, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    assert_close_layer(bf16_to_f64(torch.cat([ref[r][0] for r in range(G)])), ref_l0)
+    del graphs
+    g.close()
+
+
+def test_group_detects_mismatched_placements(cuda_ok):
+    """Call discipline: ranks dispatching with different maps are
+    caught on the device (the placement hash travels with the counts)."""
+    moe = _moe()
+    G, T, H, F, E, k = 2, 200, 64, 128, 8, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=3, with_weights=False)
+    g = Group(G, T, H, F, E, k)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    Ps = [np.array([0, 0, 0, 0, 1, 1, 1, 1]), np.array([1, 1, 1, 1, 0, 0, 0, 0])]
+    for r in range(G):
+        g.lays[r].placement(Ps[r])
+    torch.cuda.synchronize()
+    rw = g.each(lambda r, lay: lay.route(ls[r], k))
+    g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], Ps[r]))
+    for lay in g.lays:
+        with pytest.raises(moe.MoeError) as ei:
+            lay.sync()
+        assert "different expert_to_rank" in str(ei.value)
+    g.close()

@@ -171,9 +171,10 @@ def test_empty_and_invalid_inputs(cuda_ok):
     lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 3, 3])
     out = lay.combine(torch.zeros(0, 2, device=DEV))
     assert out.shape == (0, 64)
+    lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 3, 4])          # placement value >= G: device-validated
     with pytest.raises(moe.MoeError) as ei:
-        lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 3, 4])      # placement value >= G
-    assert ei.value.status == 1
+        lay.sync()
+    assert ei.value.status == 6 and "expert_to_rank value" in str(ei.value)
     with pytest.raises(moe.MoeError) as ei:
         lay.route(torch.zeros(65, 8, device=DEV), 2)          # T > max_tokens
     assert ei.value.status == 4
@@ -380,14 +381,12 @@ def test_timeline_events_ordered(cuda_ok):
         assert all(b >= a for a, b in zip(main, main[1:]))
 
 
-@pytest.mark.parametrize("ksplit,ksplit5", [("1", "1"), ("3", "2"), ("8", "4")])
-def test_decode_splitk(cuda_ok, ksplit, ksplit5, monkeypatch):
-    """Decode-sized contexts split K6 over F and K5 over H (fp32 partials, ordered
-    reduction; K5's SwiGLU applied in the reduction); forced slice counts,
-    including slices of a single k-block, against the oracle."""
+@pytest.mark.parametrize("ksplit", ["1", "3", "8"])
+def test_decode_splitk(cuda_ok, ksplit, monkeypatch):
+    """Decode-sized contexts split K6 over F (fp32 partials, ordered reduction);
+    forced slice counts, including slices of a single k-block, against the oracle."""
     monkeypatch.setenv("MOE_GEMM_CG", "1")
     monkeypatch.setenv("MOE_DECODE_SPLITK", ksplit)
-    monkeypatch.setenv("MOE_DECODE_SPLITK5", ksplit5)
     T, H, F, E, k, G = 301, 256, 512, 8, 2, 2
     P = [1, 0, 1, 1, 0, 1, 0, 1]
     inp = Inputs(T, H, F, E, k, s=1.6, seed=37)
@@ -395,3 +394,50 @@ def test_decode_splitk(cuda_ok, ksplit, ksplit5, monkeypatch):
     out, idx, w = run_layer(lay, inp, P, G)
     ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
     assert_close_layer(bf16_to_f64(out), ref)
+
+
+def test_device_placement_is_validated_on_the_device(cuda_ok):
+    """moe_dispatch takes the placement as a device array; a value
+    outside [0, G) latches MOE_ERR_DEVICE (and is read as 0, so no buffer index
+    leaves its bounds); the next dispatch with a valid map is unaffected."""
+    moe = _moe()
+    T, H, F, E, k, G = 300, 64, 128, 8, 2, 4
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=41)
+    lay = make_layer(T, H, F, E, k, G)
+    x, logits = inp.to_device(DEV)
+    idx, w = lay.route(logits, k)
+    bad = torch.tensor([0, 1, 2, 4, 3, 2, 1, 0], dtype=torch.int32, device=DEV)
+    lay.dispatch(x, idx, bad)
+    with pytest.raises(moe.MoeError) as ei:
+        lay.sync()
+    assert ei.value.status == 6 and "expert_to_rank value" in str(ei.value)
+    good = torch.tensor([0, 1, 2, 3, 3, 2, 1, 0], dtype=torch.int32, device=DEV)
+    out, _, _ = run_layer(lay, inp, good, G)
+    ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    assert_close_layer(bf16_to_f64(out), ref)
+
+
+def test_weight_count_mismatch_is_caught(cuda_ok):
+    """moe_expert_ffn's n_w must equal the experts the placement hosts: the host
+    cannot see a device placement, so the GEMM checks it (MOE_ERR_DEVICE)."""
+    moe = _moe()
+    T, H, F, E, k = 200, 64, 128, 8, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=43)
+    lay = make_layer(T, H, F, E, k, 1)
+    x, logits = inp.to_device(DEV)
+    idx, w = lay.route(logits, k)
+    lay.dispatch(x, idx, [0] * E)
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E - 1)))      # one expert short
+    lay.expert_ffn(moe.pack_w13(w1, w3), w2)
+    lay.combine(w)
+    with pytest.raises(moe.MoeError) as ei:
+        lay.sync()
+    assert ei.value.status == 6 and "n_w" in str(ei.value)
+    vl = make_layer(T, H, F, E, k, 2)                                # virtual ranks: n_w == E, host-checked
+    vi, vw = vl.route(logits, k)
+    vl.dispatch(x, vi, [0, 1] * 4)
+    with pytest.raises(moe.MoeError) as ei:
+        vl.expert_ffn(moe.pack_w13(w1, w3), w2)
+    assert ei.value.status == 1
+    vl.close()
+    lay.close()

@@ -141,6 +141,7 @@ def test_tp_bad_configs(cuda_ok):
     lay = moe.MoeLayer(ffn=256, virtual_ranks=4, tp=2, **kw)
     x = torch.zeros(8, 64, dtype=torch.bfloat16, device=DEV)
     idx = torch.zeros(8, 2, dtype=torch.int32, device=DEV)
-    with pytest.raises(moe.MoeError) as ei:                   # placement value >= G/tp groups
-        lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 0, 0])
-    assert ei.value.status == 1
+    lay.dispatch(x, idx, [0, 0, 1, 1, 2, 2, 0, 0])            # placement value >= G/tp groups
+    with pytest.raises(moe.MoeError) as ei:                   # (device-validated: latched)
+        lay.sync()
+    assert ei.value.status == 6 and "expert_to_rank value" in str(ei.value)
