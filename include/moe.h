@@ -203,6 +203,30 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
                         const int32_t* expert_to_rank, moe_dispatch_info* info,
                         moe_stream_t stream);
 
+/* ---- NEXT-4: direct layer l -> l+1 dispatch (Eq. 8; reading G11) -------
+ * Eq. 8 models token traffic from the GPU hosting a token's layer-l expert to the
+ * GPU hosting its layer-(l+1) expert.  Home-rank EP (moe_combine, then the next
+ * moe_dispatch from the token's home) never puts that traffic on the wire; this
+ * pair of calls does.  moe_set_output_mode(prev, MOE_OUT_STAY) before layer l's
+ * moe_expert_ffn keeps layer l's expert outputs on the hosting ranks (no
+ * moe_combine for that layer).  moe_dispatch_from(ctx, prev, w_prev, idx, T, k,
+ * expert_to_rank) then dispatches layer l+1 (ctx, another context of the same
+ * rank and EP group; idx and expert_to_rank as in moe_dispatch) without a
+ * hidden-state row: every rank hosting a layer-(l+1) expert of token t forms its
+ * receive row itself as
+ *     x_{l+1}[t] = bf16( sum_{j ascending} w_prev[t][j] * Y_l[item (t, j)] )
+ * (G4: fp32 FMA, one bf16 rounding -- bit-identical to the home-rank combine),
+ * reading Y_l where layer l computed it: locally when both experts share a GPU
+ * (what ILP 2 arranges), over NVLink otherwise.  The source sends only 12 bytes
+ * per routed row and layer-l item (slot, row, weight).  w_prev: float [T][k_l]
+ * (layer l's gate weights, device).  T must equal layer l's T on this rank.
+ * Collective like moe_dispatch; P2P, virtual ranks or one rank; tp == 1.  The
+ * last layer of a chain returns home with moe_combine (MOE_OUT_HOME, default). */
+typedef enum { MOE_OUT_HOME = 0, MOE_OUT_STAY = 1 } moe_output_mode;
+moe_status moe_set_output_mode(moe_ctx_t ctx, int32_t mode);
+moe_status moe_dispatch_from(moe_ctx_t ctx, moe_ctx_t prev, const float* w_prev, const int32_t* idx, int32_t T,
+                             int32_t k, const int32_t* expert_to_rank, moe_stream_t stream);
+
 /* ---- a6: grouped SwiGLU expert FFN (G5) ---------------------------------
  * For every hosted expert e and its received rows X_e:
  *   h = bf16( silu(X_e W1_e^T) * (X_e W3_e^T) ),  Y_e = bf16( h W2_e^T )
@@ -266,7 +290,8 @@ moe_status moe_layout_host(int32_t E, int32_t G, const int32_t* P, const int32_t
  * of that call (any pointer may be NULL):
  *   dest_rank [T][k]  rank (EP group when tp > 1) hosting item (t, j)'s expert
  *   recv_pos  [T][k]  unpadded position of the item in that rank's receive order
- *   send_slot [T][k]  position of the item in its source's send order (C3 slot)
+ *   send_slot [T][k]  position of the item in its source's send order (C3 slot), as
+ *                     computed by the device (the fused combine's return slot)
  *   cnt       [G][E]  count matrix of all ranks. */
 moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos,
                           int32_t* send_slot, int32_t* cnt);
@@ -275,6 +300,13 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos,
  * returns the rows and the other slices zeros), for bit-exact dispatch/combine
  * tests (out must equal x). */
 moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream);
+
+/* MOE_A2A_NCCL mode: copies the compact send buffer of the last dispatch -- this
+ * rank's rows for remote experts, in the C3 send order (key P[e], e, t; G9) -- to
+ * host bf16 [rows][H] (rows_host may be NULL to query *rows_out).  Other modes
+ * have no send buffer (MOE_ERR_UNSUPPORTED): P2P stores rows straight into the
+ * peers' receive buffers, virtual ranks into the shared receive buffer. */
+moe_status moe_debug_send(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out);
 
 /* Copies the received rows of the last dispatch, in unpadded receive order of
  * this process (virtual: rank 0's rows first, ...), to host bf16 [rows][H]. */

@@ -66,12 +66,13 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 // arrives (a rank that skipped a collective call, a dead process) latches
 // kErrTimeout after kFlagTimeoutNs instead of hanging the GPU.
 __device__ __forceinline__ unsigned cur_epoch(const unsigned* p) { return *(volatile const unsigned*)p; }
-__device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch, int* err) {
+__device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch, int* err,
+                                               unsigned long long timeout_ns) {
   for (int g = threadIdx.x; g < n; g += blockDim.x) {
     const uint64_t t0 = globaltimer_ns();
     while ((int)(ld_acquire_sys(flags + g) - epoch) < 0) {
       __nanosleep(64);
-      if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
         atomicOr(err, kErrTimeout);
         break;
       }
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(1024) k_scan(PlanArgs a, PlanBuffers b) {
 // first item of (source s, expert e); NCCL mode sends remote items through a
 // compact send buffer in key (P[e], e) order instead.
 __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers b, long long cap_rows) {
-  __shared__ int rows_s[kMaxExperts], pad_s[kMaxExperts], p_s[kMaxExperts];
+  __shared__ int rows_s[kMaxExperts], pad_s[kMaxExperts], p_s[kMaxExperts], key_e[kMaxExperts];
   const int e = threadIdx.x;
   const int E = a.E;
   const int* cnt = b.cnt_all;
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
     }
     __syncthreads();
     if (threadIdx.x == 0) signal_all(a, b, 0);
-    wait_flags_geq(b.my_sig->flag_cnt, a.G, cur_epoch(a.epoch_ptr), b.err);
+    wait_flags_geq(b.my_sig->flag_cnt, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns);
     for (int g = threadIdx.x; g < a.G; g += blockDim.x)
       if (((volatile unsigned*)b.my_sig->phash)[g] != my_hash) atomicOr(b.err, kErrPlacement);
     cnt = b.my_sig->cnt;
@@ -269,14 +270,10 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
       }
       b.base_row[s * E + e] = base;
     }
+    key_e[pos_v] = e;  // experts in send-order key (P[e], e) order (for cslot_base below)
     if (a.p2p) {
-      // fused combine: C3 send-order slot bases.  cslot_base[e] = first slot of this
-      // rank's items of expert e; for each hosted segment and source s: the rows of s
-      // inside the segment and the slot of their first item in s's send order.
-      int sb = 0;
-      for (int q = 0; q < E; ++q)
-        if (p_s[q] * E + q < key) sb += ((volatile const int*)cnt)[a.me * E + q];
-      b.cslot_base[e] = sb;
+      // fused combine: for each hosted segment and source s, the rows of s inside the
+      // segment and the C3 send-order slot of their first item in s's send order
       if (hosted) {
         long long row = rstart;
         for (int s = 0; s < a.G; ++s) {
@@ -291,6 +288,20 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
           row += n;
         }
       }
+    }
+  }
+  // C3 send order of every local source s (G9: key (P[e], e), then token): the slot of
+  // the first item of (s, e) is the count of s's items with a smaller key.  Thread s
+  // walks the experts in key order.  (P2P: the fused combine's return slots; every
+  // mode: moe_debug_plan reports these device-computed slots.)
+  __syncthreads();
+  for (int sl = threadIdx.x; sl < a.V; sl += blockDim.x) {
+    const int gs = a.virt ? sl : a.me;
+    int acc = 0;
+    for (int pos = 0; pos < E; ++pos) {
+      const int q = key_e[pos];
+      b.cslot_base[sl * E + q] = acc;
+      acc += ((volatile const int*)cnt)[gs * E + q];
     }
   }
   if (e == 0) {
@@ -356,14 +367,14 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
         const int within = b.tile_base[(long long)tile * E + e] + r;  // stable rank among (s, e) items
         row = b.base_row[s * E + e] + within;
         slot = item_slot(a, b.P[e]);
-        if (a.p2p) cslot = b.cslot_base[e] + within;
+        cslot = b.cslot_base[s * E + e] + within;
       }
       it.row[i] = row;
       it.slot[i] = (uint8_t)slot;
       if (write_plan) {
         b.row_of_item[(long long)t0 * a.k + i] = row;
         b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
-        if (a.p2p) b.cslot_of_item[(long long)t0 * a.k + i] = cslot;
+        b.cslot_of_item[(long long)t0 * a.k + i] = cslot;
       }
     }
     __syncthreads();
@@ -399,6 +410,48 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   int s, t0, t1, tile0;
   tile_info(a, tile, s, t0, t1, tile0);
   tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && (mode == 0 || mode == 1));
+  if (mode == 6) {
+    // direct dispatch: instead of x rows, every destination row gets the locations and
+    // gate weights of the k layer-l expert outputs it combines
+    const int n = (t1 - t0) * a.k;
+    const int pk = b.prev_k;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int row = it.row[i];
+      if (row < 0) continue;
+      const long long gt = t0 + i / a.k;
+      int32_t* d = b.desc_table[a.virt || !a.p2p ? 0 : it.slot[i]] + (long long)row * b.desc_k * 3;
+      for (int j = 0; j < pk; ++j) {
+        const long long gi = gt * pk + j;
+        const int pr = b.prev_row[gi];
+        d[3 * j] = b.prev_slot[gi];
+        d[3 * j + 1] = pr;
+        d[3 * j + 2] = __float_as_int(pr < 0 ? 0.f : b.prev_w[gi]);
+      }
+    }
+    __syncthreads();
+    continue;
+  }
+  if (mode == 5) {
+    // gather dispatch: the rows travel as whole token blocks (copy engines); tell each
+    // receiving rank which token-buffer row every one of its rows from here is
+    const int n = (t1 - t0) * a.k;
+    const int tr = a.me * (int)b.tok_rows;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int row = it.row[i];
+      if (row < 0) continue;
+      const int trow = tr + t0 + i / a.k;
+      if (a.tp == 1) {
+        if (it.slot[i] != a.me) b.xmap_table[it.slot[i]][row] = trow;
+      } else {
+        for (int q = 0; q < a.tp; ++q) {
+          const int r = it.slot[i] * a.tp + q;
+          if (r != a.me) b.xmap_table[r][row] = trow;
+        }
+      }
+    }
+    __syncthreads();
+    continue;
+  }
   // P2P, tp > 1: slot p (an EP group) fans out to ranks p*tp .. p*tp+tp-1 (the TP
   // all-gather inside the dispatch); otherwise a slot is one destination buffer
   const bool fan = a.p2p && a.tp > 1;
@@ -454,7 +507,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   }
   __syncthreads();  // it / run are reused by the next work unit
   }
-  if (a.p2p && (mode == 0 || mode == 2)) {
+  if (a.p2p && (mode == 0 || mode == 2 || mode == 5 || mode == 6)) {
     // the last CTA to finish raises flag_data[me] on every rank
     __threadfence_system();
     __syncthreads();
@@ -464,6 +517,136 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
       *b.done_counter = 0;
       signal_all(a, b, 1);
     }
+  }
+}
+
+// ----------------------------------------------------------------- gather dispatch: expand
+// The receiving side of the gather dispatch.  Source by source (rotated from
+// me + 1), once flag_data[s] says s's token block and row map have landed: every
+// row of every hosted segment that came from s is copied from the token buffer
+// (row xmap[row]) into the receive layout, one warp per row, 16-byte vectors.
+// The last CTA done with a source raises flag_exp[s] (K5's per-tile wait).
+__global__ void __launch_bounds__(kScatterThreads) k_expand(PlanArgs a, PlanBuffers b) {
+  __shared__ unsigned last;
+  const unsigned epoch = cur_epoch(a.epoch_ptr);
+  const int nseg = b.seg_meta_c[0];
+  const int cpr = a.H / 8;
+  const int lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + (threadIdx.x >> 5), stride = gridDim.x * nw;
+  for (int q = 1; q < a.G; ++q) {
+    const int s = (a.me + q) % a.G;
+    if (threadIdx.x == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      while ((int)(ld_acquire_sys(&b.my_sig->flag_data[s]) - epoch) < 0) {
+        __nanosleep(128);
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicOr(b.err, kErrTimeout);
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    for (int pos = 0; pos < nseg; ++pos) {
+      const int32_t* d = b.seg_src + ((long long)pos * a.G + s) * 3;
+      const int row0 = d[0], n = d[1];
+      for (int r = gw; r < n; r += stride) {
+        const long long row = row0 + r;
+        const uint4* src = b.tok_local + (long long)b.xmap_local[row] * cpr;
+        uint4* dst = b.recv_local + row * cpr;
+        for (int c = lane; c < cpr; c += 32) dst[c] = src[c];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&b.exp_counter[s], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      b.exp_counter[s] = 0;
+      __threadfence();
+      st_release_sys(&b.my_sig->flag_exp[s], epoch);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st_release_sys(&b.my_sig->flag_exp[a.me], epoch);
+}
+
+// ----------------------------------------------------------------- direct dispatch: combine here
+// NEXT-4 (the inter-layer traffic Eq. 8 models): the rows of layer l+1
+// are formed on the rank hosting their layer-(l+1) expert, straight from layer l's
+// expert outputs where they were computed (a local read when ILP 2 put the two
+// experts on one GPU, an NVLink load otherwise) -- no return to the home rank.
+// Same arithmetic as K8 (fp32 FMA, j ascending, one bf16 rounding), so the layer
+// input is bit-identical to the home-rank chain's.
+__global__ void __launch_bounds__(kScatterThreads) k_expand_direct(PlanArgs a, PlanBuffers b) {
+  __shared__ const uint4* src_s[kMaxWorld];
+  __shared__ unsigned last;
+  const int nslots = a.p2p ? a.G : 1;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = b.prev_src[q];
+  if (a.p2p && threadIdx.x == 0) {
+    const unsigned ep = cur_epoch(a.epoch_ptr), pep = cur_epoch(b.prev_epoch);
+    const uint64_t t0 = globaltimer_ns();
+    for (int g = 0; g < a.G; ++g) {   // every source's descriptors and every rank's layer-l outputs
+      while ((int)(ld_acquire_sys(&b.my_sig->flag_data[g]) - ep) < 0 ||
+             (int)(ld_acquire_sys(b.prev_flag_y + g) - pep) < 0) {
+        __nanosleep(128);
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicOr(b.err, kErrTimeout);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int E = a.E, cpr = a.H / 8, pk = b.prev_k, dk = b.desc_k;
+  const int nseg = b.seg_meta_c[0];
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + (threadIdx.x >> 5), stride = gridDim.x * nw;
+  for (int pos = 0; pos < nseg; ++pos) {
+    const int row0 = b.seg_meta_c[1 + pos], n = b.seg_meta_c[1 + E + pos];
+    for (int r = gw; r < n; r += stride) {
+      const long long row = row0 + r;
+      const int32_t* d = b.desc_local + row * dk * 3;
+      for (int c = lane; c < cpr; c += 32) {
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+        for (int j = 0; j < pk; ++j) {
+          const int prow = d[3 * j + 1];
+          if (prow < 0) continue;
+          const float wj = __int_as_float(d[3 * j + 2]);
+          const uint4 v = src_s[d[3 * j]][(long long)prow * cpr + c];
+          acc[0] = fmaf(wj, bf16_lo(v.x), acc[0]);
+          acc[1] = fmaf(wj, bf16_hi(v.x), acc[1]);
+          acc[2] = fmaf(wj, bf16_lo(v.y), acc[2]);
+          acc[3] = fmaf(wj, bf16_hi(v.y), acc[3]);
+          acc[4] = fmaf(wj, bf16_lo(v.z), acc[4]);
+          acc[5] = fmaf(wj, bf16_hi(v.z), acc[5]);
+          acc[6] = fmaf(wj, bf16_lo(v.w), acc[6]);
+          acc[7] = fmaf(wj, bf16_hi(v.w), acc[7]);
+        }
+        uint4 o;
+        o.x = pack_bf16x2(acc[0], acc[1]);
+        o.y = pack_bf16x2(acc[2], acc[3]);
+        o.z = pack_bf16x2(acc[4], acc[5]);
+        o.w = pack_bf16x2(acc[6], acc[7]);
+        b.recv_local[row * cpr + c] = o;
+      }
+    }
+  }
+  if (!a.p2p) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&b.exp_counter[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    b.exp_counter[0] = 0;
+    __threadfence();
+    const unsigned ep = cur_epoch(a.epoch_ptr);
+    for (int g = 0; g < a.G; ++g) st_release_sys(&b.my_sig->flag_exp[g], ep);
   }
 }
 
@@ -504,7 +687,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_combine(PlanArgs a, cons
     w_s[i] = v < 0 ? 0.f : w[gi];
     slot_s[i] = a.fused ? 0 : b.slot_of_item[gi];
   }
-  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, cur_epoch(a.epoch_ptr), b.err);
+  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns);
   __syncthreads();
   const int cpr = a.H / 8;
   const int cw = (cpr + a.col_split - 1) / a.col_split;
@@ -641,22 +824,37 @@ void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cu
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
                     cudaStream_t s, int max_ctas) {
   const size_t smem = sizeof(int) * (kScatterThreads / 32) * a.E;
-  int grid = a.n_tiles * a.col_split;
+  int grid = a.n_tiles * (mode >= 5 ? 1 : a.col_split);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  if (a.n_tiles > 0)
-    k_scatter<<<grid, kScatterThreads, smem, s>>>(a, (const uint4*)x, idx, b, mode);
-  else if (a.p2p && (mode == 0 || mode == 2))
+  if (a.n_tiles > 0) {
+    if (mode >= 5) {  // one CTA per token tile (no column slices: no rows are copied)
+      PlanArgs a1 = a;
+      a1.col_split = 1;
+      k_scatter<<<grid, kScatterThreads, smem, s>>>(a1, (const uint4*)x, idx, b, mode);
+    } else {
+      k_scatter<<<grid, kScatterThreads, smem, s>>>(a, (const uint4*)x, idx, b, mode);
+    }
+  } else if (a.p2p && (mode == 0 || mode == 2 || mode == 5 || mode == 6)) {
     k_signal<<<1, 32, 0, s>>>(a, b, 1);
+  }
 }
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s) {
   k_signal<<<1, 32, 0, s>>>(a, b, which);
 }
-__global__ void k_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err) {
-  wait_flags_geq(flags, n, cur_epoch(epoch_ptr), err);
+__global__ void k_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, unsigned long long tmo) {
+  wait_flags_geq(flags, n, cur_epoch(epoch_ptr), err, tmo);
 }
-void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, cudaStream_t s) {
-  k_wait<<<1, 64, 0, s>>>(flags, n, epoch_ptr, err);
+void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, unsigned long long timeout_ns,
+                 cudaStream_t s) {
+  k_wait<<<1, 64, 0, s>>>(flags, n, epoch_ptr, err, timeout_ns);
 }
+void launch_expand_direct(const PlanArgs& a, const PlanBuffers& b, int max_ctas, cudaStream_t s) {
+  k_expand_direct<<<max_ctas > 0 ? max_ctas : 32, kScatterThreads, 0, s>>>(a, b);
+}
+void launch_expand(const PlanArgs& a, const PlanBuffers& b, int max_ctas, cudaStream_t s) {
+  k_expand<<<max_ctas > 0 ? max_ctas : 32, kScatterThreads, 0, s>>>(a, b);
+}
+
 __global__ void k_expect_nseg(const int32_t* seg_meta, int n, int* err) {
   if (seg_meta[0] != n) atomicOr(err, kErrWeights);
 }
@@ -687,7 +885,8 @@ void preload_dispatch_kernels() {
   const void* fs[] = {(const void*)k_count, (const void*)k_scan, (const void*)k_layout, (const void*)k_scatter,
                       (const void*)k_signal, (const void*)k_wait, (const void*)k_expect_nseg,
                       (const void*)k_combine<0>, (const void*)k_combine<1>, (const void*)k_combine<2>,
-                      (const void*)k_combine<4>, (const void*)k_combine<8>, (const void*)k_pack_w13};
+                      (const void*)k_combine<4>, (const void*)k_combine<8>, (const void*)k_pack_w13,
+                      (const void*)k_expand, (const void*)k_expand_direct};
   for (const void* f : fs) cudaFuncGetAttributes(&fa, f);
 }
 

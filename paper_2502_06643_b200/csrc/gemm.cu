@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       sg.wrow[i] = seg_meta[1 + 2 * E + i] * N;
       sg.mtiles[i] = mt;
       int a0 = 0, a1 = 0;
-      if (sw.flags != nullptr) {  // M tiles lying inside this rank's own rows [lo, hi)
+      if (sw.flags != nullptr && sw.me >= 0) {  // M tiles lying inside this rank's own rows [lo, hi)
         const int32_t* own = sw.seg_src + ((long long)i * sw.G + sw.me) * 3;
         const int lo = own[0] - sg.row0[i], hi = lo + own[1];
         if (own[1] > 0) {
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             unsigned v;
             do {
               asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sw.flags + s) : "memory");
-              if (globaltimer_ns() - t0 > kFlagTimeoutNs) {
+              if (globaltimer_ns() - t0 > sw.timeout_ns) {
                 atomicOr(err, kErrTimeout);
                 break;
               }

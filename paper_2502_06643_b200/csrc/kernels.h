@@ -18,6 +18,8 @@ struct SigBlock {
   unsigned flag_data[64];     // flag_data[s] = epoch once every row s sends here landed
   unsigned flag_y[64];        // flag_y[g] = epoch once rank g's expert outputs are ready
   unsigned phash[64];         // phash[s] = hash of the placement source s dispatched with
+  unsigned flag_exp[64];      // gather dispatch: flag_exp[s] = epoch once this rank expanded source
+                              // s's token rows into its receive layout (local flag; [me] too)
 };
 
 // Dispatch plan arguments shared by K2/K3/K8 (dispatch.cu).
@@ -39,6 +41,11 @@ struct PlanArgs {
   int col_split;  // K3/K8: CTAs per token tile, each copying a slice of the hidden dim
   int seg_align;  // expert segments are padded to this many rows (= the GEMM M tile, 128 or 256)
   int fused;      // K8 reads the local return buffer at the C3 slot (fused-combine mode)
+  int gather;     // P2P gather dispatch: token rows reach the peers by copy engine, rows are
+                  // expanded into the expert-major layout on the receiver (k_expand)
+  unsigned long long timeout_ns;  // bound on every P2P flag wait (latches MOE_ERR_TIMEOUT)
+  int direct;     // direct layer l -> l+1 dispatch (moe_dispatch_from): the receive rows are
+                  // combined on the hosting rank from layer l's expert outputs (k_expand_direct)
 };
 
 // Device-side plan state (allocated by the context).
@@ -62,12 +69,34 @@ struct PlanBuffers {
   // fused combine (P2P): K6 stores each expert-output row straight into the
   // source rank's return buffer at the item's send-order slot (C3 slot)
   int32_t* seg_src;               // [E][G][3]: per hosted segment and source: first row, rows, first slot
-  int32_t* cslot_base;            // [E] send-order slot of this rank's first item for expert e
-  int32_t* cslot_of_item;         // [T*k] send-order slot (C3) of every item of this rank
+  int32_t* cslot_base;            // [V][E] send-order slot of local source s's first item for expert e
+  int32_t* cslot_of_item;         // [T*k] send-order slot (C3) of every item (within its source)
   const uint4* ret_local;         // this rank's return buffer
   // tp > 1: the tp partial outputs of one item live part_stride uint4 apart (virtual
   // mode: the expert-output buffers of the slices; fused combine: the return buffers)
   long long part_stride;
+  // gather dispatch (P2P): every source's token block lands in tok [G][tok_rows][H] of every
+  // peer (copy engines); the source writes, for each of its rows a peer receives, the token
+  // buffer row into that peer's xmap [cap_rows]; the peer's k_expand copies the rows
+  uint4* recv_local;              // this rank's receive buffer
+  const uint4* tok_local;         // this rank's token buffer
+  const int32_t* xmap_local;      // this rank's row -> token-buffer row map
+  int32_t* const* xmap_table;     // [G] every rank's xmap
+  unsigned* exp_counter;          // [G] k_expand last-CTA detection per source
+  long long tok_rows;             // token-buffer rows per source (max_tokens)
+  const int32_t* seg_meta_c;      // segment table (nseg at [0]) for k_expand
+  // direct layer l -> l+1 dispatch: per receive row, prev_k descriptors {slot, row, w} of
+  // the layer-l expert-output rows it combines (desc [cap_rows][desc_k][3] int32 per rank)
+  int32_t* const* desc_table;     // [G] every rank's descriptor buffer (virtual: [0] = own)
+  const int32_t* desc_local;
+  int desc_k;                     // descriptor slots per row (the context's max_k)
+  const int32_t* prev_row;        // layer l's row_of_item [T*prev_k] (this rank)
+  const uint8_t* prev_slot;       // layer l's slot_of_item (hosting rank / buffer slot)
+  const float* prev_w;            // layer l's gate weights [T][prev_k]
+  int prev_k;
+  const uint4* const* prev_src;   // layer l's expert-output buffers by slot (this rank's table)
+  const unsigned* prev_flag_y;    // layer l's flag_y in this rank's layer-l signal block (P2P)
+  const unsigned* prev_epoch;     // layer l's flag epoch
 };
 
 // K5 per-tile arrival waits (P2P overlap): the producer waits only for the source
@@ -78,6 +107,7 @@ struct SrcWait {
   int G;
   int me;
   const unsigned* epoch_ptr;      // see PlanArgs::epoch_ptr
+  unsigned long long timeout_ns;  // see PlanArgs::timeout_ns
 };
 
 // K6 epilogue redirection (fused combine, P2P mode); enabled == 0 -> plain stores.
@@ -100,14 +130,24 @@ int plan_tiles(int T, int V);
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
 void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s);
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s);
-// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers
+// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers,
+// 5 = gather dispatch: only the row -> token-buffer map entries of the peers' rows,
+// 6 = direct dispatch: the combine descriptors of every row (all destinations, own included)
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
                     cudaStream_t s, int max_ctas = 0);  // max_ctas > 0: persistent grid of that size
 void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uint16_t* out, cudaStream_t s);
+// Direct dispatch: every receive row = bf16(sum_j w_j * Y_l[slot_j][row_j]) (fp32 FMA, j
+// ascending -- the home-rank combine's arithmetic); P2P: after every source's descriptors
+// (flag_data) and every rank's layer-l outputs (layer-l flag_y) arrived; raises flag_exp.
+void launch_expand_direct(const PlanArgs& a, const PlanBuffers& b, int max_ctas, cudaStream_t s);
+// Gather dispatch: expand every peer's token rows (token buffer -> receive layout),
+// source by source as each source's flag_data arrives; raises flag_exp per source.
+void launch_expand(const PlanArgs& a, const PlanBuffers& b, int max_ctas, cudaStream_t s);
 // P2P: raise flag `which` (0 cnt, 1 data, 2 y) = epoch on every rank, after a system fence.
 void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStream_t s);
 // P2P: wait until flags[0..n) >= epoch (system-scope acquire).
-void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, cudaStream_t s);
+void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, unsigned long long timeout_ns,
+                 cudaStream_t s);
 // Latch kErrWeights unless the last layout hosts exactly n expert segments here.
 void launch_expect_nseg(const int32_t* seg_meta, int n, int* err, cudaStream_t s);
 void launch_pack_w13(const uint16_t* w1, const uint16_t* w3, int n, int F, int H, uint16_t* w13,

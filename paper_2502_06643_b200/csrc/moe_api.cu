@@ -115,6 +115,25 @@ struct moe_ctx {
   // 6.59 (128) in one run (profiles/r1_v13_timeline_ctas_*); Mixtral 4EP unchanged.
   // MOE_SCATTER_CTAS overrides.
   int remote_ctas = 32;
+  // gather dispatch (P2P): with top-k >= G/tp most tokens reach most
+  // ranks, so every token block is copied once to every peer by the copy engines
+  // (no SM time, host-known sizes), only a 4-byte row -> token index crosses per
+  // routed row, and the receiver expands its rows locally (k_expand).  Default for
+  // k >= G / tp; MOE_DISPATCH=scatter|gather overrides.
+  uint16_t* tokbuf = nullptr;           // [G][max_tokens][H]: every source's token block
+  int32_t* xmap = nullptr;              // [cap_rows]: receive row -> token-buffer row
+  int32_t** xmap_table = nullptr;       // device [G]
+  unsigned* exp_counter = nullptr;      // [G]
+  std::vector<void*> tok_peer;          // host [G]: every rank's token buffer (peer pointers)
+  bool last_gather = false;             // the last dispatch used the gather path
+  // direct layer l -> l+1 dispatch (NEXT-4): combine descriptors [cap_rows][max_k][3]
+  // of this rank's receive rows (written by the sources), peers' tables
+  int32_t* desc = nullptr;
+  int32_t** desc_table = nullptr;       // device [max(G, 1)]
+  bool last_direct = false;             // the last dispatch was moe_dispatch_from
+  bool out_stay = false;                // MOE_OUT_STAY: outputs stay for moe_dispatch_from
+  bool ffn_done = false;                // moe_expert_ffn ran after the last dispatch
+  unsigned long long flag_timeout_ns = kFlagTimeoutNs;  // MOE_FLAG_TIMEOUT_MS overrides
   // single-process group (moe_ctx_create_group): every rank's context lives in this
   // process; the peer tables hold the other contexts' device pointers directly (no
   // IPC, no NCCL).  shared_dev: another rank of the group runs on the same device --
@@ -196,6 +215,16 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.cslot_of_item = c->cslot_of_item;
   b.ret_local = reinterpret_cast<const uint4*>(c->retbuf);
   b.part_stride = c->virt ? c->cap_rows * c->H / 8 : c->send_rows * c->H / 8;
+  b.recv_local = reinterpret_cast<uint4*>(c->recv);
+  b.tok_local = reinterpret_cast<const uint4*>(c->tokbuf);
+  b.xmap_local = c->xmap;
+  b.xmap_table = c->xmap_table;
+  b.exp_counter = c->exp_counter;
+  b.tok_rows = c->cfg.max_tokens;
+  b.seg_meta_c = c->seg_meta;
+  b.desc_table = c->desc_table;
+  b.desc_local = c->desc;
+  b.desc_k = c->cfg.max_k;
   return b;
 }
 
@@ -216,6 +245,9 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.n_tiles = plan_tiles(T, c->V);
   a.seg_align = c->seg_align;
   a.fused = c->p2p && c->ffn_fused;
+  a.gather = 0;
+  a.direct = 0;
+  a.timeout_ns = c->flag_timeout_ns;
   // enough CTAs for the HBM/NVLink-bound row copies, but no partial second wave:
   // K3/K8 CTAs (512 threads) fit twice per SM, so aim at <= 2 x num_sms CTAs
   const int chunks = c->H / 8;
@@ -378,6 +410,8 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "loading the kernels: %s", cudaGetErrorString(e));
   }
+  if (const char* ft = getenv("MOE_FLAG_TIMEOUT_MS"))
+    ctx->flag_timeout_ns = std::max(1ull, (unsigned long long)atoll(ft)) * 1000000ull;
   if (share > 1) {
     // ranks sharing one device: each gets an equal slice of the SMs for its persistent
     // grids, 16 SMs stay free for the peers' row copies, so a GEMM CTA waiting for a
@@ -433,10 +467,12 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
             A((void**)&ctx->peer_sig, sizeof(void*) * (size_t)G) &&
             A((void**)&ctx->sig, sizeof(SigBlock)) && A((void**)&ctx->done_counter, 4 * sizeof(unsigned)) &&
             A((void**)&ctx->seg_src, sizeof(int32_t) * 3 * (size_t)E * G) &&
-            A((void**)&ctx->cslot_base, sizeof(int32_t) * (size_t)E) &&
+            A((void**)&ctx->cslot_base, sizeof(int32_t) * (size_t)ctx->V * E) &&
             A((void**)&ctx->cslot_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
             A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G) &&
-            A((void**)&ctx->epoch_dev, sizeof(unsigned));
+            A((void**)&ctx->epoch_dev, sizeof(unsigned)) &&
+            A((void**)&ctx->desc, sizeof(int32_t) * 3 * (size_t)k * ctx->cap_rows) &&
+            A((void**)&ctx->desc_table, sizeof(void*) * (size_t)std::max(G, 1));
   if (!ok) return MOE_ERR_CUDA;
   cudaMemset(ctx->sig, 0, sizeof(SigBlock));
   cudaMemset(ctx->done_counter, 0, 4 * sizeof(unsigned));  // [0] scatter last-CTA, [2..3] GEMM scheduler
@@ -467,11 +503,19 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
   return MOE_OK;
 }
 
-// P2P mode: the side stream of the peers' row copies and its fork / join events.
+// P2P mode: the side stream of the peers' row copies and its fork / join events,
+// and the gather dispatch's token buffer and row map.
 static moe_status p2p_streams(moe_ctx_t ctx) {
   ctx->p2p = true;
   if (const char* rc = getenv("MOE_SCATTER_CTAS")) ctx->remote_ctas = atoi(rc);
   CU(cudaSetDevice(ctx->cfg.device));
+  const size_t tok_bytes = (size_t)ctx->G * std::max(ctx->cfg.max_tokens, 1) * ctx->H * 2;
+  CU(cudaMalloc((void**)&ctx->tokbuf, tok_bytes));
+  CU(cudaMalloc((void**)&ctx->xmap, sizeof(int32_t) * (size_t)ctx->cap_rows));
+  CU(cudaMalloc((void**)&ctx->xmap_table, sizeof(void*) * (size_t)ctx->G));
+  CU(cudaMalloc((void**)&ctx->exp_counter, sizeof(unsigned) * (size_t)ctx->G));
+  CU(cudaMemset(ctx->exp_counter, 0, sizeof(unsigned) * (size_t)ctx->G));
+  ctx->tok_peer.assign(ctx->G, nullptr);
   CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
@@ -519,7 +563,8 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       return bail(MOE_ERR_NCCL);
     }
   }
-  std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr), ret(G, nullptr);
+  std::vector<void*> dst(std::max(G, 2)), src(std::max(G, 2)), sig(G, nullptr), ret(G, nullptr), xm;
+  std::vector<void*> dsc(1, ctx->desc);   // NCCL / virtual / one rank: slot 0 = own
   ret[0] = ctx->retbuf;
   dst[0] = ctx->recv;
   dst[1] = ctx->sendbuf;
@@ -531,9 +576,11 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     // handles are exchanged once here over NCCL
     st = p2p_streams(ctx);
     if (st != MOE_OK) return bail(st);
-    cudaIpcMemHandle_t h[4];
+    cudaIpcMemHandle_t h[7];
     if (cudaIpcGetMemHandle(&h[0], ctx->recv) != cudaSuccess || cudaIpcGetMemHandle(&h[1], ctx->ybuf) != cudaSuccess ||
-        cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess || cudaIpcGetMemHandle(&h[3], ctx->retbuf) != cudaSuccess) {
+        cudaIpcGetMemHandle(&h[2], ctx->sig) != cudaSuccess || cudaIpcGetMemHandle(&h[3], ctx->retbuf) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h[4], ctx->tokbuf) != cudaSuccess || cudaIpcGetMemHandle(&h[5], ctx->xmap) != cudaSuccess ||
+        cudaIpcGetMemHandle(&h[6], ctx->desc) != cudaSuccess) {
       fail(ctx, MOE_ERR_CUDA, "cudaIpcGetMemHandle failed");
       return bail(MOE_ERR_CUDA);
     }
@@ -549,17 +596,22 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       return bail(MOE_ERR_NCCL);
     }
     cudaFree(dh);
+    xm.assign(G, nullptr);
+    dsc.assign(G, nullptr);
     for (int g = 0; g < G; ++g) {
       if (g == c.rank) {
         dst[g] = ctx->recv;
         src[g] = ctx->ybuf;
         sig[g] = ctx->sig;
         ret[g] = ctx->retbuf + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
+        ctx->tok_peer[g] = ctx->tokbuf;
+        xm[g] = ctx->xmap;
+        dsc[g] = ctx->desc;
         continue;
       }
       const cudaIpcMemHandle_t* hg = reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + hb * g);
-      void* p[4] = {nullptr, nullptr, nullptr, nullptr};
-      for (int i = 0; i < 4; ++i) {
+      void* p[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      for (int i = 0; i < 7; ++i) {
         cudaError_t e = cudaIpcOpenMemHandle(&p[i], hg[i], cudaIpcMemLazyEnablePeerAccess);
         if (e != cudaSuccess) {
           fail(ctx, MOE_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", g, cudaGetErrorString(e));
@@ -572,7 +624,18 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
       sig[g] = p[2];
       // fused combine of TP slice tpi lands in partial region tpi of the source's buffer
       ret[g] = static_cast<uint16_t*>(p[3]) + (size_t)ctx->tpi * ctx->send_rows * c.hidden;
+      ctx->tok_peer[g] = p[4];
+      xm[g] = p[5];
+      dsc[g] = p[6];
     }
+  }
+  if (cudaMemcpy(ctx->desc_table, dsc.data(), sizeof(void*) * dsc.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    fail(ctx, MOE_ERR_CUDA, "descriptor table upload failed");
+    return bail(MOE_ERR_CUDA);
+  }
+  if (ctx->p2p && cudaMemcpy(ctx->xmap_table, xm.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+    fail(ctx, MOE_ERR_CUDA, "xmap table upload failed");
+    return bail(MOE_ERR_CUDA);
   }
   st = upload_tables(ctx, dst, src, sig, ret);
   if (st != MOE_OK) return bail(st);
@@ -637,12 +700,21 @@ moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t*
     }
   for (int r = 0; r < n; ++r) {
     moe_ctx_t c = cs[r];
-    std::vector<void*> dst(n), src(n), sig(n), ret(n);
+    std::vector<void*> dst(n), src(n), sig(n), ret(n), xm(n), dsc(n);
     for (int g = 0; g < n; ++g) {
       dst[g] = cs[g]->recv;
       src[g] = cs[g]->ybuf;
       sig[g] = cs[g]->sig;
       ret[g] = cs[g]->retbuf + (size_t)c->tpi * cs[g]->send_rows * c->H;
+      c->tok_peer[g] = cs[g]->tokbuf;
+      xm[g] = cs[g]->xmap;
+      dsc[g] = cs[g]->desc;
+    }
+    cudaSetDevice(c->cfg.device);
+    if (cudaMemcpy(c->xmap_table, xm.data(), sizeof(void*) * n, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->desc_table, dsc.data(), sizeof(void*) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
+      fail(c, MOE_ERR_CUDA, "xmap table upload failed");
+      return bail(MOE_ERR_CUDA, c);
     }
     moe_status st = upload_tables(c, dst, src, sig, ret);
     if (st != MOE_OK) return bail(st, c);
@@ -686,7 +758,8 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
                  ctx->base_row, ctx->seg_meta, ctx->row_of_item, ctx->err_dev, ctx->recv, ctx->hbuf, ctx->ybuf,
                  ctx->sendbuf, ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig,
                  ctx->sig, ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
-                 ctx->epoch_dev, ctx->splitk_ws};
+                 ctx->epoch_dev, ctx->splitk_ws, ctx->tokbuf, ctx->xmap, ctx->xmap_table, ctx->exp_counter,
+                 ctx->desc, ctx->desc_table};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -795,16 +868,14 @@ moe_status moe_pack_w13(const moe_bf16* w1, const moe_bf16* w3, int32_t n, int32
   return MOE_OK;
 }
 
-moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
-                        const int32_t* expert_to_rank, moe_dispatch_info* info, moe_stream_t stream) {
-  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
-  if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
-  if (k < 1 || k > ctx->E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
-  if (!expert_to_rank) return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank is NULL");
-  if (T > 0 && (!x || !idx)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+// moe_dispatch (prev == NULL) and moe_dispatch_from (prev = layer l's context: the
+// rows are combined from layer l's expert outputs on the hosting ranks, NEXT-4).
+static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
+                                const int32_t* expert_to_rank, moe_dispatch_info* info, cudaStream_t s,
+                                moe_ctx_t prev, const float* w_prev) {
   const int E = ctx->E, G = ctx->G, H = ctx->H;
+  const bool direct = prev != nullptr;
   const int n_grp = G / ctx->tp;  // EP ranks (groups of tp ranks when tp > 1)
-  cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   CU(cudaSetDevice(ctx->cfg.device));
 
@@ -828,9 +899,39 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     }
     ctx->cur_join = ev_join;
   }
+  // gather dispatch (see moe_ctx::tokbuf): top-k >= G/tp, or MOE_DISPATCH
+  bool gather = ctx->p2p && k >= n_grp;
+  if (const char* dm = getenv("MOE_DISPATCH")) gather = ctx->p2p && !strcmp(dm, "gather");
+  if (direct) gather = false;
+  ctx->last_gather = gather;
+  ctx->last_direct = direct;
+  if (gather && T > 0) {
+    // this rank's token block goes to every peer's token buffer (region `me`) on the
+    // copy engines, overlapping the plan kernels.  Safe to overwrite: every peer read
+    // the previous layer's block before raising the flag_y this rank's last combine
+    // waited for.
+    CU(cudaEventRecord(ev_fork, s));
+    CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
+    const size_t bytes = (size_t)T * H * 2;
+    for (int g = 0; g < G; ++g)
+      if (g != ctx->me)
+        CU(cudaMemcpyAsync(static_cast<uint16_t*>(ctx->tok_peer[g]) + (size_t)ctx->me * ctx->cfg.max_tokens * H, x,
+                           bytes, cudaMemcpyDeviceToDevice, ctx->side));
+  }
   PlanArgs a = plan_args(ctx, T, k);
+  a.gather = gather ? 1 : 0;
+  a.direct = direct ? 1 : 0;
   PlanBuffers b = plan_buffers(ctx);
   b.P_in = expert_to_rank;
+  if (direct) {
+    b.prev_row = prev->row_of_item;
+    b.prev_slot = prev->slot_of_item;
+    b.prev_w = w_prev;
+    b.prev_k = prev->last_k;
+    b.prev_src = prev->src_table;
+    b.prev_flag_y = prev->sig->flag_y;
+    b.prev_epoch = prev->epoch_dev;
+  }
   launch_count(a, idx, b, s);
   launch_scan(a, b, s);
   LAUNCHED(ctx, (a.n_tiles > 0) + 1);
@@ -861,12 +962,40 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   }
   launch_layout(a, b, ctx->cap_rows, s);  // validates P; P2P: also the in-kernel count all-gather
   tl_rec(ctx, 1, s);
-  if (ctx->p2p) {
+  if (direct && !ctx->p2p) {
+    // virtual ranks / one rank: descriptors, then every receive row combined in place
+    launch_scatter(a, x, idx, b, 6, s);
+    launch_expand_direct(a, b, 2 * ctx->num_sms, s);
+    tl_rec(ctx, 2, s);
+    tl_rec(ctx, 3, s);
+    LAUNCHED(ctx, 2);
+  } else if (direct) {
+    // side stream: every row's combine descriptors to its hosting rank (flag_data),
+    // then this rank's rows combined from the layer-l outputs once every source's
+    // descriptors and every rank's layer-l outputs are there (flag_exp for K5)
+    CU(cudaEventRecord(ev_fork, s));
+    CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
+    launch_scatter(a, x, idx, b, 6, ctx->side);
+    launch_expand_direct(a, b, ctx->remote_ctas, ctx->side);
+    tl_rec(ctx, 3, ctx->side);
+    CU(cudaEventRecord(ev_join, ctx->side));
+    tl_rec(ctx, 2, s);
+    LAUNCHED(ctx, 2);
+  } else if (ctx->p2p) {
     // rows for peers: NVLink stores on the side stream (arrival flags raised by its
     // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
     CU(cudaEventRecord(ev_fork, s));
     CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-    launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
+    if (gather) {
+      // side stream: the row -> token-row map entries of the peers' rows (raising
+      // flag_data after the block copies above), then this rank's expansion of the
+      // rows its peers sent, source by source as they arrive
+      launch_scatter(a, x, idx, b, 5, ctx->side);
+      launch_expand(a, b, ctx->remote_ctas, ctx->side);
+      LAUNCHED(ctx, 1);
+    } else {
+      launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
+    }
     tl_rec(ctx, 3, ctx->side);
     CU(cudaEventRecord(ev_join, ctx->side));
     launch_scatter(a, x, idx, b, 1, s);
@@ -907,6 +1036,7 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
     NC(ncclGroupEnd());
   }
   ctx->have_plan = true;
+  ctx->ffn_done = false;
   ctx->last_T = T;
   ctx->last_k = k;
   ctx->last_tiles = a.n_tiles;
@@ -941,6 +1071,45 @@ moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, in
   return MOE_OK;
 }
 
+moe_status moe_dispatch(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
+                        const int32_t* expert_to_rank, moe_dispatch_info* info, moe_stream_t stream) {
+  if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
+  if (k < 1 || k > ctx->E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
+  if (!expert_to_rank) return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank is NULL");
+  if (T > 0 && (!x || !idx)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  return dispatch_impl(ctx, x, idx, T, k, expert_to_rank, info, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+moe_status moe_dispatch_from(moe_ctx_t ctx, moe_ctx_t prev, const float* w_prev, const int32_t* idx, int32_t T,
+                             int32_t k, const int32_t* expert_to_rank, moe_stream_t stream) {
+  if (!ctx || !prev) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx / prev is NULL");
+  if (ctx == prev) return fail(ctx, MOE_ERR_INVALID_ARG, "prev must be another context (layer l's outputs stay in it)");
+  if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
+  if (k < 1 || k > ctx->E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
+  if (!expert_to_rank) return fail(ctx, MOE_ERR_INVALID_ARG, "expert_to_rank is NULL");
+  if (T > 0 && (!idx || !w_prev)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  if (!prev->have_plan || !prev->out_stay || !prev->ffn_done)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "prev needs moe_set_output_mode(prev, MOE_OUT_STAY) and its moe_expert_ffn");
+  if (prev->last_T != T) return fail(ctx, MOE_ERR_INVALID_ARG, "prev dispatched %d tokens, not %d", prev->last_T, T);
+  if (prev->last_k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "prev's k exceeds this context's max_k");
+  if (prev->H != ctx->H || prev->G != ctx->G || prev->virt != ctx->virt || prev->p2p != ctx->p2p ||
+      prev->me != ctx->me || prev->cfg.device != ctx->cfg.device)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "prev must be the same rank of the same EP group (H, G, mode, device)");
+  if (ctx->tp > 1 || prev->tp > 1) return fail(ctx, MOE_ERR_UNSUPPORTED, "direct dispatch with tp > 1");
+  if (ctx->comm && !ctx->p2p) return fail(ctx, MOE_ERR_UNSUPPORTED, "direct dispatch needs MOE_A2A_P2P");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (prev->p2p) CU(cudaStreamWaitEvent(s, prev->cur_join, 0));  // layer l's side stream is done with its plan
+  return dispatch_impl(ctx, nullptr, idx, T, k, expert_to_rank, nullptr, s, prev, w_prev);
+}
+
+moe_status moe_set_output_mode(moe_ctx_t ctx, int32_t mode) {
+  if (!ctx || (mode != MOE_OUT_HOME && mode != MOE_OUT_STAY)) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
+  if (mode == MOE_OUT_STAY && ctx->tp > 1) return fail(ctx, MOE_ERR_UNSUPPORTED, "MOE_OUT_STAY with tp > 1");
+  ctx->out_stay = mode == MOE_OUT_STAY;
+  return MOE_OK;
+}
+
 moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2, int32_t n_w, moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
   if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_expert_ffn before moe_dispatch");
@@ -960,7 +1129,13 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   {
     bool fused = ctx->Fl <= 8192;
     if (const char* env = getenv("MOE_FUSED_COMBINE")) fused = atoi(env) != 0;
-    ctx->ffn_fused = ctx->p2p && fused;
+    ctx->ffn_fused = ctx->p2p && fused && !ctx->out_stay;  // MOE_OUT_STAY: the outputs stay here
+  }
+  ctx->ffn_done = true;
+  if (ctx->out_stay && ctx->p2p) {
+    // no moe_combine follows to join the side stream: K5 waited for every row it
+    // reads anyway, so join here (keeps a captured chain's streams joined)
+    CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));
   }
   if (n_w == 0) {
     // no expert here: the placement must host none on this rank (checked on the
@@ -994,8 +1169,11 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (rec) CU(cudaEventRecord(ev[0], s));
   // P2P: K5's producer waits per tile for the source ranks whose rows the tile reads;
   // the tiles of this rank's own rows go first (overlapping the peers' NVLink pushes)
-  const SrcWait wait1{ctx->p2p ? ctx->sig->flag_data : nullptr, ctx->seg_src, ctx->G, ctx->me, ctx->epoch_dev};
-  const SrcWait nowait{nullptr, nullptr, 0, 0, nullptr};
+  const unsigned* arrived = (ctx->last_gather || ctx->last_direct) ? ctx->sig->flag_exp : ctx->sig->flag_data;
+  // (direct dispatch: this rank's own rows are combined by k_expand_direct too -- wait for all)
+  const SrcWait wait1{ctx->p2p ? arrived : nullptr, ctx->seg_src, ctx->G, ctx->last_direct ? -1 : ctx->me,
+                      ctx->epoch_dev, ctx->flag_timeout_ns};
+  const SrcWait nowait{nullptr, nullptr, 0, 0, nullptr, 0};
   const FusedRet plain{nullptr, nullptr, 0, 0};
   // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
   // source rank's return buffer at the item's send-order slot -- the combine
@@ -1141,7 +1319,8 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
     // join the side-stream scatter first (never spin on a flag another kernel of
     // this GPU raises), then wait for the peers' rows
     CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));
-    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch_dev, ctx->err_dev, s);
+    launch_wait((ctx->last_gather || ctx->last_direct) ? ctx->sig->flag_exp : ctx->sig->flag_data, ctx->G,
+                ctx->epoch_dev, ctx->err_dev, ctx->flag_timeout_ns, s);
     LAUNCHED(ctx, 1);
   }
   const size_t ybytes = (size_t)ctx->cap_rows * ctx->H * 2;
@@ -1159,6 +1338,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
   if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_combine before moe_dispatch");
   if (ctx->last_T > 0 && (!w || !out)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
+  if (ctx->out_stay) return fail(ctx, MOE_ERR_INVALID_ARG, "MOE_OUT_STAY: the outputs go to moe_dispatch_from");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   const int E = ctx->E, G = ctx->G, H = ctx->H;
@@ -1198,7 +1378,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
     // done -- and every peer raises flag_y only after that.  Ranks sharing a device
     // wait with one CTA here instead of with every CTA of the combine (those would
     // hold the SMs a peer's expert GEMM needs to raise the flag).
-    launch_wait(ctx->sig->flag_y, ctx->G, ctx->epoch_dev, ctx->err_dev, s);
+    launch_wait(ctx->sig->flag_y, ctx->G, ctx->epoch_dev, ctx->err_dev, ctx->flag_timeout_ns, s);
     LAUNCHED(ctx, 1);
   }
   launch_combine(a, w, b, out, s);
@@ -1224,19 +1404,21 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
   std::vector<int32_t> cnt((size_t)G * E), rows((size_t)std::max(1, T * k)), Pv(E);
   CU(cudaMemcpy(Pv.data(), ctx->P_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost));
   std::vector<uint8_t> slots((size_t)std::max(1, T * k));
+  std::vector<int32_t> cslots((size_t)std::max(1, T * k));
   const int32_t* cnt_dev = plan_buffers(ctx).cnt_all;
   CU(cudaMemcpy(cnt.data(), cnt_dev, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost));
   if (T * k) {
     CU(cudaMemcpy(rows.data(), ctx->row_of_item, sizeof(int32_t) * T * k, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(slots.data(), ctx->slot_of_item, (size_t)T * k, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(cslots.data(), ctx->cslot_of_item, sizeof(int32_t) * T * k, cudaMemcpyDeviceToHost));
   }
   // P2P: per-rank padded layout of the destination rank
   std::vector<int32_t> peer_base((size_t)G * E);
   layout_host_impl(E, G, Pv.data(), cnt.data(), ctx->seg_align, nullptr, peer_base.data(), nullptr, nullptr);
   if (cnt_out) memcpy(cnt_out, cnt.data(), sizeof(int32_t) * G * E);
   const int32_t* P = Pv.data();
-  // unpadded receive start of (e, s) on rank P[e]; send-order base of (s, e)
-  std::vector<int64_t> ustart((size_t)G * E), sbase((size_t)G * E), cbase(E);
+  // unpadded receive start of (e, s) on rank P[e]
+  std::vector<int64_t> ustart((size_t)G * E);
   for (int g = 0; g < G; ++g) {
     int64_t acc = 0;
     for (int e = 0; e < E; ++e) {
@@ -1246,15 +1428,6 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
         acc += cnt[(size_t)s * E + e];
       }
     }
-  }
-  for (int s = 0; s < G; ++s) {
-    int64_t acc = 0;
-    for (int g = 0; g < G; ++g)
-      for (int e = 0; e < E; ++e)
-        if (P[e] == g) {
-          sbase[(size_t)s * E + e] = acc;
-          acc += cnt[(size_t)s * E + e];
-        }
   }
   // padded device receive base of (s, e): virtual mode concatenates every rank's
   // segments in key (P[e], e) order; real mode uses this rank's own buffer.
@@ -1323,7 +1496,7 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
             const int64_t rank_within = row - b0;
             dr = P[e];
             rp = (int32_t)(ustart[(size_t)s * E + e] + rank_within);
-            ss = (int32_t)(sbase[(size_t)s * E + e] + rank_within);
+            ss = cslots[(size_t)t * k + j];  // the device's own C3 send-order slot
             break;
           }
         }
@@ -1336,12 +1509,29 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
   return MOE_OK;
 }
 
+moe_status moe_debug_send(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out) {
+  if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
+  if (!(ctx->comm && !ctx->p2p)) return fail(ctx, MOE_ERR_UNSUPPORTED, "the compact send buffer exists in MOE_A2A_NCCL mode only");
+  CU(cudaSetDevice(ctx->cfg.device));
+  CU(cudaStreamSynchronize(ctx->last_stream));
+  const int E = ctx->E, H = ctx->H;
+  int64_t n = 0;
+  for (int e = 0; e < E; ++e)
+    if (ctx->P_host[e] != ctx->grp) n += ctx->cnt_host[(size_t)ctx->me * E + e];
+  if (rows_out) *rows_out = n;
+  if (!rows_host) return MOE_OK;
+  if (n > max_rows) return fail(ctx, MOE_ERR_CAPACITY, "max_rows too small (%lld)", (long long)n);
+  if (n) CU(cudaMemcpy(rows_host, ctx->sendbuf, (size_t)n * H * 2, cudaMemcpyDeviceToHost));
+  return MOE_OK;
+}
+
 moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out) {
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   CU(cudaSetDevice(ctx->cfg.device));
   if (ctx->p2p) {  // the peers' rows of the last dispatch have landed here
     CU(cudaStreamWaitEvent(ctx->last_stream, ctx->cur_join, 0));
-    launch_wait(ctx->sig->flag_data, ctx->G, ctx->epoch_dev, ctx->err_dev, ctx->last_stream);
+    launch_wait((ctx->last_gather || ctx->last_direct) ? ctx->sig->flag_exp : ctx->sig->flag_data, ctx->G,
+                ctx->epoch_dev, ctx->err_dev, ctx->flag_timeout_ns, ctx->last_stream);
   }
   CU(cudaStreamSynchronize(ctx->last_stream));
   const int E = ctx->E, H = ctx->H;

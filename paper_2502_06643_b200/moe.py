@@ -23,8 +23,8 @@ STATUS = {0: "MOE_OK", 1: "MOE_ERR_INVALID_ARG", 2: "MOE_ERR_CUDA", 3: "MOE_ERR_
 # Every symbol include/moe.h declares (checked by tests/test_abi_cpu.py).
 EXPORTS = ["moe_get_unique_id", "moe_ctx_create", "moe_ctx_create_group", "moe_ctx_destroy", "moe_ctx_sync", "moe_status_str",
            "moe_last_error", "moe_abi_version", "moe_route", "moe_route_stats", "moe_stats_allreduce", "moe_stats_allreduce_layers",
-           "moe_dispatch", "moe_expert_ffn", "moe_combine", "moe_pack_w13", "moe_placement_contiguous",
-           "moe_layout_host", "moe_debug_plan", "moe_debug_identity_ffn", "moe_debug_recv", "moe_kernel_launches",
+           "moe_dispatch", "moe_dispatch_from", "moe_set_output_mode", "moe_expert_ffn", "moe_combine", "moe_pack_w13", "moe_placement_contiguous",
+           "moe_layout_host", "moe_debug_plan", "moe_debug_identity_ffn", "moe_debug_recv", "moe_debug_send", "moe_kernel_launches",
            "moe_ffn_timing_enable", "moe_ffn_timing_read", "moe_timeline_enable", "moe_timeline_read"]
 
 
@@ -64,6 +64,8 @@ def load_library(path=LIB_PATH):
         "moe_stats_allreduce_layers": [P, P, P, I32, I32, P],
         "moe_dispatch": [P, P, P, I32, I32, P, P, P],
         "moe_expert_ffn": [P, P, P, I32, P],
+        "moe_dispatch_from": [P, P, P, P, I32, I32, P, P],
+        "moe_set_output_mode": [P, I32],
         "moe_combine": [P, P, P, P],
         "moe_pack_w13": [P, P, I32, I32, I32, P, P],
         "moe_placement_contiguous": [I32, I32, P],
@@ -71,6 +73,7 @@ def load_library(path=LIB_PATH):
         "moe_debug_plan": [P, P, P, P, P],
         "moe_debug_identity_ffn": [P, P],
         "moe_debug_recv": [P, P, I64, P],
+        "moe_debug_send": [P, P, I64, P],
         "moe_ffn_timing_enable": [P, I32],
         "moe_ffn_timing_read": [P, P, I32, P],
         "moe_timeline_enable": [P, I32],
@@ -335,6 +338,23 @@ class MoeLayer:
         self._last = (T, k)
         return inf
 
+    def dispatch_from(self, prev, w_prev, idx, expert_to_rank, stream=None):
+        """NEXT-4 direct dispatch (moe.h, moe_dispatch_from): this layer's receive rows
+        are combined on the hosting ranks from layer `prev`'s expert outputs (prev:
+        the MoeLayer of layer l on this rank, run with output_mode("stay"))."""
+        T, k = idx.shape
+        d = self.device
+        P = self.placement(expert_to_rank)
+        self._c(_lib.moe_dispatch_from(self._ctx, prev._ctx, _dev(w_prev, torch.float32, d, "w_prev", 2),
+                                       _dev(idx, torch.int32, d, "idx", 2), T, k,
+                                       _dev(P, torch.int32, d, "expert_to_rank", 1), _stream(stream)))
+        self._last = (T, k)
+
+    def output_mode(self, mode):
+        """"home" (default: moe_combine returns the outputs) or "stay" (they stay on the
+        hosting ranks for the next layer's dispatch_from)."""
+        self._c(_lib.moe_set_output_mode(self._ctx, {"home": 0, "stay": 1}[mode]))
+
     # a6
     def expert_ffn(self, w13, w2, stream=None):
         """w13 bf16 [n_w][2F][H] (pack_w13), w2 bf16 [n_w][H][F]: the experts the last
@@ -372,4 +392,12 @@ class MoeLayer:
         self._c(_lib.moe_debug_recv(self._ctx, None, 0, ctypes.byref(n)))
         buf = np.zeros((max(n.value, 1), self.H), np.uint16)
         self._c(_lib.moe_debug_recv(self._ctx, _np_ptr(buf), n.value, ctypes.byref(n)))
+        return buf[:n.value]
+
+    def debug_send(self):
+        """NCCL mode: this rank's compact send buffer (remote rows in C3 send order)."""
+        n = ctypes.c_int64()
+        self._c(_lib.moe_debug_send(self._ctx, None, 0, ctypes.byref(n)))
+        buf = np.zeros((max(n.value, 1), self.H), np.uint16)
+        self._c(_lib.moe_debug_send(self._ctx, _np_ptr(buf), n.value, ctypes.byref(n)))
         return buf[:n.value]

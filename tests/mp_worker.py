@@ -67,8 +67,17 @@ def main():
         assert np.array_equal(ss, pl["slot"][rank]), "send slots"
         assert np.array_equal(rp, pl["recv_pos"][rank]), "receive positions"
         assert np.array_equal(dr, P[ridx[a:b]]), "destination ranks"
-        rows = lay.debug_recv()
         xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+        if lay.a2a == "nccl":
+            # the device's compact send buffer, row by row, in the oracle's C3 send
+            # order (G9) restricted to remote destinations
+            sl = pl["slot"][rank]
+            mine = ridx[a:b]
+            items = sorted(((int(sl[t, j]), t) for t in range(b - a) for j in range(k)
+                            if P[mine[t, j]] != rank))
+            ref_send = xb[[a + t for _, t in items]].reshape(-1, H)
+            assert np.array_equal(lay.debug_send(), ref_send), "send buffer order"
+        rows = lay.debug_recv()
         ref_rows = xb[[blocks[s][0] + t for (s, t, j, e) in pl["recv"][rank]]].reshape(-1, H)
         assert np.array_equal(rows, ref_rows), "received payload"
         lay.identity_ffn()

@@ -93,10 +93,16 @@ PLACEMENTS = {
 }
 
 
+@pytest.mark.parametrize("dispatch", ["scatter", "gather"])
 @pytest.mark.parametrize("fused", ["0", "1"])
 @pytest.mark.parametrize("G", [2, 4])
-def test_group_plan_payload_and_layer(cuda_ok, G, fused, monkeypatch):
+def test_group_plan_payload_and_layer(cuda_ok, G, fused, dispatch, monkeypatch):
+    """scatter: every routed row is stored into the hosting rank's receive row by
+    the source (NVLink); gather: every token block is copied once to every peer by
+    the copy engines, the source sends only the row -> token map, and the receiver
+    expands its rows (k_expand); fused / pulled combine."""
     monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
+    monkeypatch.setenv("MOE_DISPATCH", dispatch)
     moe = _moe()
     T, H, F, E, k = 1500, 256, 512, 8, 2
     inp = Inputs(T, H, F, E, k, s=1.6, seed=21 + G)
@@ -149,12 +155,15 @@ def test_group_plan_payload_and_layer(cuda_ok, G, fused, monkeypatch):
     g.close()
 
 
-@pytest.mark.parametrize("G,tp,fused", [(2, 2, "0"), (2, 2, "1"), (4, 2, "1"), (4, 4, "0")])
-def test_group_tensor_parallel(cuda_ok, G, tp, fused, monkeypatch):
+@pytest.mark.parametrize("G,tp,fused,dispatch", [(2, 2, "0", "scatter"), (2, 2, "1", "gather"),
+                                                 (4, 2, "1", "scatter"), (4, 2, "0", "gather"),
+                                                 (4, 4, "0", "scatter")])
+def test_group_tensor_parallel(cuda_ok, G, tp, fused, dispatch, monkeypatch):
     """EP x TP over G ranks of one GPU (reading G20): the TP all-gather fan-out of
     the dispatch and the bf16 partial return of the combine, against the oracle's
     TP layer and the virtual-rank TP run."""
     monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
+    monkeypatch.setenv("MOE_DISPATCH", dispatch)
     moe = _moe()
     T, H, F, E, k = 1100, 256, 512, 8, 2
     n_grp = G // tp
@@ -340,3 +349,120 @@ def test_group_detects_mismatched_placements(cuda_ok):
             lay.sync()
         assert "different expert_to_rank" in str(ei.value)
     g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_group_topk_at_least_ranks_default_gather(cuda_ok, G):
+    """The D5 regime (top-k >= EP ranks: E16 top-4 here, E64 top-8 in the bench)
+    takes the gather dispatch by default; uneven experts per rank (G14); plan,
+    payload, layer vs virtual ranks and the oracle."""
+    moe = _moe()
+    T, H, F, E, k = 900, 128, 256, 16, 4
+    P = np.array([(3 * e + e // 5) % G for e in range(E)])
+    inp = Inputs(T, H, F, E, k, s=1.2, seed=71 + G)
+    g = Group(G, T, H, F, E, k)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    ridx, _ = oroute.route(inp.logits.numpy(), k)
+    xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+    ws = []
+    for r in range(G):
+        hosted = [e for e in range(E) if P[e] == r]
+        w1, w3, w2 = inp.device_weights(DEV, hosted)
+        ws.append((moe.pack_w13(w1, w3), w2) if hosted else (None, None))
+        g.lays[r].placement(P)
+    torch.cuda.synchronize()
+    for rep in range(2):
+        rw = g.each(lambda r, lay: lay.route(ls[r], k))
+        g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        if rep == 0:
+            pl = oplan.plan([ridx[a:b] for a, b in g.blocks], P, G)
+            for r, lay in enumerate(g.lays):
+                dr, rp, ss, cnt = lay.debug_plan()
+                assert np.array_equal(cnt, pl["cnt"]) and np.array_equal(ss, pl["slot"][r])
+                assert np.array_equal(rp, pl["recv_pos"][r])
+                ref_rows = xb[[g.blocks[s][0] + t for (s, t, j, e) in pl["recv"][r]]].reshape(-1, H)
+                assert np.array_equal(lay.debug_recv(), ref_rows)
+        g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
+        outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+        g.sync()
+        out = torch.cat(outs)
+        if rep == 0:
+            virt = _virtual_out(inp, P, G, k)
+            ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+        assert torch.equal(out.view(torch.int16), virt.view(torch.int16))
+        assert_close_layer(bf16_to_f64(out), ref)
+    g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_group_direct_layer_to_layer_dispatch(cuda_ok, G):
+    """NEXT-4 over real P2P ranks (one GPU): a 4-layer chain with per-layer
+    placements, direct l -> l+1 dispatch (each rank's receive rows combined from
+    the layer-l outputs where they were computed: local reads for co-located
+    experts, peer loads otherwise) vs the home-rank chain -- bit-identical."""
+    moe = _moe()
+    T, H, F, E, k, L = 800, 128, 256, 8, 2, 4
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=61 + G)
+    blocks = oplan.token_blocks(T, G)
+    tmax = max(b - a for a, b in blocks)
+    mk = lambda: moe.MoeLayer.group(G, max_tokens=tmax, hidden=H, ffn=F, num_experts=E, max_k=k)
+    home, ca, cb = mk(), mk(), mk()
+    streams = [torch.cuda.Stream(device=DEV) for _ in range(G)]
+    x_all = inp.x.to(DEV)
+    xs = [x_all[a:b].contiguous() for a, b in blocks]
+    lg = [synth_logits(T, E, 100 + li) for li in range(L)]
+    ls = [[q[a:b].contiguous() for a, b in blocks] for q in lg]
+    plans = [np.array(p) % G for p in ([0, 0, 1, 1, 2, 2, 3, 3], [0, 1, 2, 2, 3, 2, 3, 3], [1, 0, 3, 2, 0, 1, 2, 3],
+                                       [3, 3, 2, 2, 1, 1, 0, 0])]
+    w1a, w3a, w2a = inp.device_weights(DEV, list(range(E)))
+    ws = {}
+    for li, P in enumerate(plans):
+        for r in range(G):
+            hosted = [e for e in range(E) if P[e] == r]
+            sel = torch.tensor(hosted, device=DEV, dtype=torch.long)
+            ws[li, r] = (moe.pack_w13(w1a[sel], w3a[sel]), w2a[sel].contiguous()) if hosted else (None, None)
+            for grp_ in (home, ca, cb):
+                grp_[r].placement(P)
+    torch.cuda.synchronize()
+
+    def each(lays, fn):
+        out = []
+        for r, lay in enumerate(lays):
+            with torch.cuda.stream(streams[r]):
+                out.append(fn(r, lay))
+        return out
+
+    # home-rank chain
+    x = xs
+    for li in range(L):
+        rw = each(home, lambda r, lay: lay.route(ls[li][r], k))
+        each(home, lambda r, lay: lay.dispatch(x[r], rw[r][0], plans[li]))
+        each(home, lambda r, lay: lay.expert_ffn(*ws[li, r]))
+        x = each(home, lambda r, lay: lay.combine(rw[r][1]))
+    torch.cuda.synchronize()
+    home_out = torch.cat(x)
+    # direct chain: two context groups alternate
+    prev = prev_w = None
+    for li in range(L):
+        cur = (ca, cb)[li % 2]
+        rw = each(cur, lambda r, lay: lay.route(ls[li][r], k))
+        if prev is None:
+            each(cur, lambda r, lay: lay.dispatch(xs[r], rw[r][0], plans[li]))
+        else:
+            each(cur, lambda r, lay: lay.dispatch_from(prev[r], prev_w[r], rw[r][0], plans[li]))
+        each(cur, lambda r, lay: lay.output_mode("home" if li == L - 1 else "stay"))
+        each(cur, lambda r, lay: lay.expert_ffn(*ws[li, r]))
+        prev, prev_w = cur, [q[1] for q in rw]
+    outs = each(prev, lambda r, lay: lay.combine(prev_w[r]))
+    for lay in prev:
+        lay.sync()
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs).view(torch.int16), home_out.view(torch.int16))
+    for grp_ in (home, ca, cb):
+        for lay in grp_:
+            lay.close()
+
+
+def synth_logits(T, E, seed):
+    import synth
+    return synth.zipf_logits(T, E, 1.6, seed=seed).to(DEV)

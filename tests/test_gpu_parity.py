@@ -247,25 +247,57 @@ def test_placement_invariance_bit_exact(cuda_ok):
         assert torch.equal(o, outs[0])
 
 
-def test_mixtral_layer_full_size_sampled(cuda_ok):
-    """BASELINE configs[1] shape at N=1 (the bench's workload: E8 k2 H4096 F14336,
-    T = 16384 tokens, all experts on one GPU), checked on sampled tokens against
-    the oracle's direct definition."""
+def tile_cover_tokens(ridx, E, tile, seed):
+    """Tokens such that every M tile of every expert segment holds a checked row.
+
+    The receive layout puts expert e's rows in one segment ordered by (source,
+    token) -- i.e. by token, since sources own contiguous token blocks (G7, G9) --
+    padded to the GEMM M tile, so routed row i of expert e lies in M tile i // tile.
+    A checked output row of token t covers, for each of its k experts, that
+    expert's K5 and K6 M tile across every N tile (the row's full h and y).  One
+    pseudo-random token per (expert, M tile) plus the first and last token."""
+    rng = np.random.default_rng(seed)
+    T = ridx.shape[0]
+    sel = {0, T - 1}
+    for e in range(E):
+        toks = np.nonzero((ridx == e).any(1))[0]
+        for m0 in range(0, len(toks), tile):
+            chunk = toks[m0:m0 + tile]
+            sel.add(int(chunk[rng.integers(0, len(chunk))]))
+    sel = np.array(sorted(sel))
+    for e in range(E):                     # assert the coverage claimed above
+        toks = np.nonzero((ridx == e).any(1))[0]
+        pos = np.searchsorted(toks, sel[np.isin(sel, toks)])
+        assert set((pos // tile).tolist()) == set(range((len(toks) + tile - 1) // tile)), e
+    return sel
+
+
+@pytest.mark.parametrize("G,P,s", [
+    (1, [0] * 8, 1.6),                            # the bench's N = 1 workload
+    (4, [0, 1, 2, 2, 3, 2, 3, 3], 1.6),           # D3: ILP-1 balanced placement, 4 virtual EP ranks
+    (4, [0, 0, 1, 1, 2, 2, 3, 3], 0.0),           # D2: uniform routing, contiguous placement
+])
+def test_mixtral_layer_full_size_every_tile(cuda_ok, G, P, s):
+    """BASELINE configs[1]/[2] shape (E8 k2 H4096 F14336, T = 16384 tokens) at the
+    bench's launch configuration, checked against the oracle's direct definition
+    on tokens chosen so that every 256-row M tile of every expert segment -- hence
+    every K5 and K6 output tile -- holds at least one checked row."""
     T, H, F, E, k = 16384, 4096, 14336, 8, 2
     dev = torch.device(DEV)
     x = synth.hidden_states(T, H, seed=0, device=dev)
-    logits = synth.zipf_logits(T, E, 1.6, seed=0, device=dev)
+    logits = synth.zipf_logits(T, E, s, seed=0, device=dev)
     ws = [synth.expert_weights(e, H, F, 0, device=dev) for e in range(E)]
     moe = _moe()
-    lay = make_layer(T, H, F, E, k, 1)
+    lay = make_layer(T, H, F, E, k, G)
     idx, w = lay.route(logits, k)
-    lay.dispatch(x, idx, [0] * 8)
+    lay.dispatch(x, idx, P)
     w13 = moe.pack_w13(torch.stack([q[0] for q in ws]), torch.stack([q[1] for q in ws]))
     w2 = torch.stack([q[2] for q in ws])
     lay.expert_ffn(w13, w2)
     out = lay.combine(w)
     lay.sync()
-    sel = np.array(sorted(set(np.random.default_rng(0).integers(0, T, 48).tolist()) | {0, T - 1}))
+    gidx = idx.cpu().numpy()
+    sel = tile_cover_tokens(gidx, E, 256, seed=G)
     xs = bf16_to_f64(x[sel])
     ls = logits[sel].cpu().numpy()
     cache = {}
@@ -277,8 +309,9 @@ def test_mixtral_layer_full_size_sampled(cuda_ok):
         from oracle import ffn
         return ffn.swiglu(rows, *cache[e])[1]
     ref, ridx, rw = olayer.layer_direct(xs, ls, k, fn)
-    assert np.array_equal(idx[sel].cpu().numpy(), ridx)
+    assert np.array_equal(gidx[sel], ridx)
     assert_close_layer(bf16_to_f64(out[sel]), ref)
+    lay.close()
 
 
 def test_e64_layer_full_size_sampled(cuda_ok):
@@ -441,3 +474,61 @@ def test_weight_count_mismatch_is_caught(cuda_ok):
     assert ei.value.status == 1
     vl.close()
     lay.close()
+
+
+def _chain_home_and_direct(make, inp_list, plans, k, E, dev_ws):
+    """Run an L-layer chain twice: home-rank EP (moe_combine, then the next
+    moe_dispatch from home) and direct l -> l+1 dispatch (NEXT-4: MOE_OUT_STAY +
+    moe_dispatch_from, two contexts alternating).  Returns both final outputs."""
+    moe = _moe()
+    L = len(plans)
+    x0, logits = inp_list
+    w13, w2 = dev_ws
+    home = make()
+    x = x0
+    for li in range(L):
+        idx, w = home.route(logits[li], k)
+        home.dispatch(x, idx, plans[li])
+        home.expert_ffn(w13, w2)
+        x = home.combine(w)
+    home.sync()
+    ctxs = [make(), make()]
+    x = x0
+    prev = prev_w = None
+    for li in range(L):
+        c = ctxs[li % 2]
+        idx, w = c.route(logits[li], k)
+        if prev is None:
+            c.dispatch(x, idx, plans[li])
+        else:
+            c.dispatch_from(prev, prev_w, idx, plans[li])
+        c.output_mode("home" if li == L - 1 else "stay")
+        c.expert_ffn(w13, w2)
+        prev, prev_w = c, w
+    out = prev.combine(prev_w)
+    prev.sync()
+    return x, out
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_direct_layer_to_layer_dispatch_bit_exact(cuda_ok, G):
+    """NEXT-4 (Eq. 8's direct inter-layer traffic): a 3-layer chain with
+    per-layer placements run with direct l -> l+1 dispatch equals the home-rank
+    chain bit-exactly (the receive rows use the home combine's arithmetic) and the
+    oracle's layer-by-layer chain within tolerance (virtual ranks; real ranks in
+    tests/test_gpu_group.py)."""
+    T, H, F, E, k, L = 700, 128, 256, 8, 2, 3
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=51)
+    x0 = inp.x.to(DEV)
+    logits = [synth.zipf_logits(T, E, 1.6, seed=100 + li).to(DEV) for li in range(L)]
+    plans = [[0, 0, 1, 1, 2, 2, 3, 3], [0, 1, 2, 2, 3, 2, 3, 3], [3, 2, 1, 0, 0, 1, 2, 3]]
+    plans = [[p % G for p in q] for q in plans]
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E)))
+    moe = _moe()
+    home_out, direct_out = _chain_home_and_direct(lambda: make_layer(T, H, F, E, k, G), (x0, logits), plans, k, E,
+                                                  (moe.pack_w13(w1, w3), w2))
+    assert torch.equal(home_out.view(torch.int16), direct_out.view(torch.int16))
+    xr = bf16_to_f64(inp.x)
+    for li in range(L):
+        xr, _, _ = olayer.layer_direct(xr, logits[li].cpu().numpy(), k, inp.oracle_expert_fn())
+    assert_close_layer(bf16_to_f64(direct_out), xr)

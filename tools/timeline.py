@@ -99,7 +99,12 @@ def main():
         step()
     rec = np.array(lay.timeline_read())
     med = np.median(rec, axis=0)
-    print(json.dumps({"rank": rank, "config": a.config, "tokens": T, "placement": a.placement, "tp": tp,
+    err = None
+    try:
+        lay.sync()
+    except moe.MoeError as ex:      # e.g. a P2P flag timeout: report it with the timeline
+        err = str(ex)
+    print(json.dumps({"rank": rank, "error": err, "config": a.config, "tokens": T, "placement": a.placement, "tp": tp,
                       "env": {kk: v for kk, v in os.environ.items() if kk.startswith("MOE_")},
                       "median_ms": dict(zip(moe.MoeLayer.TIMELINE, [round(float(v), 4) for v in med]))}),
           flush=True)
