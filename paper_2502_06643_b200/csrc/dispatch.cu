@@ -409,7 +409,10 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   const int tile = unit / split;
   int s, t0, t1, tile0;
   tile_info(a, tile, s, t0, t1, tile0);
-  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && (mode == 0 || mode == 1));
+  // the plan arrays (row / slot / send slot of every item) come from the launch that
+  // covers this rank's items on the caller's stream: modes 0 and 1, or -- direct
+  // dispatch, which copies no rows -- mode 6
+  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && (mode == 0 || mode == 1 || mode == 6));
   if (mode == 6) {
     // direct dispatch: instead of x rows, every destination row gets the locations and
     // gate weights of the k layer-l expert outputs it combines
@@ -432,21 +435,47 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
     continue;
   }
   if (mode == 5) {
-    // gather dispatch: the rows travel as whole token blocks (copy engines); tell each
-    // receiving rank which token-buffer row every one of its rows from here is
+    // gather dispatch: each token row goes ONCE to every peer hosting at least one of
+    // its experts (tp > 1: every rank of those groups), into the peer's token buffer
+    // at (this source, token); the peer's row map learns which token-buffer row each
+    // of its receive rows is, and k_expand fills the receive layout locally
+    __shared__ unsigned long long tmask[kTileTokens];
     const int n = (t1 - t0) * a.k;
     const int tr = a.me * (int)b.tok_rows;
+    for (int q = threadIdx.x; q < t1 - t0; q += blockDim.x) tmask[q] = 0ull;
+    __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int row = it.row[i];
       if (row < 0) continue;
       const int trow = tr + t0 + i / a.k;
-      if (a.tp == 1) {
-        if (it.slot[i] != a.me) b.xmap_table[it.slot[i]][row] = trow;
-      } else {
-        for (int q = 0; q < a.tp; ++q) {
-          const int r = it.slot[i] * a.tp + q;
-          if (r != a.me) b.xmap_table[r][row] = trow;
-        }
+      for (int q = 0; q < a.tp; ++q) {
+        const int r = it.slot[i] * a.tp + q;
+        if (r == a.me) continue;
+        if (part == 0) b.xmap_table[r][row] = trow;
+        atomicOr(&tmask[i / a.k], 1ull << r);
+      }
+    }
+    __syncthreads();
+    const int cpr = a.H / 8;
+    const int cw = (cpr + a.col_split - 1) / a.col_split;
+    const int c_lo = part * cw;
+    const int width = max(0, min(cpr, c_lo + cw) - c_lo);
+    const long long total = (long long)(t1 - t0) * width;
+    constexpr int U = 4;
+    for (long long p0 = threadIdx.x; p0 < total; p0 += (long long)blockDim.x * U) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long p = p0 + (long long)u * blockDim.x;
+        if (p < total) v[u] = __ldg(x + (long long)(t0 + p / width) * cpr + c_lo + p % width);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long p = p0 + (long long)u * blockDim.x;
+        if (p >= total) continue;
+        const int tok = (int)(p / width), c = c_lo + (int)(p % width);
+        const long long dst = (long long)(tr + t0 + tok) * cpr + c;
+        for (unsigned long long m = tmask[tok]; m; m &= m - 1) b.tok_table[__ffsll((long long)m) - 1][dst] = v[u];
       }
     }
     __syncthreads();
@@ -824,10 +853,10 @@ void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cu
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
                     cudaStream_t s, int max_ctas) {
   const size_t smem = sizeof(int) * (kScatterThreads / 32) * a.E;
-  int grid = a.n_tiles * (mode >= 5 ? 1 : a.col_split);
+  int grid = a.n_tiles * (mode == 6 ? 1 : a.col_split);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (a.n_tiles > 0) {
-    if (mode >= 5) {  // one CTA per token tile (no column slices: no rows are copied)
+    if (mode == 6) {  // one CTA per token tile (no column slices: no rows are copied)
       PlanArgs a1 = a;
       a1.col_split = 1;
       k_scatter<<<grid, kScatterThreads, smem, s>>>(a1, (const uint4*)x, idx, b, mode);

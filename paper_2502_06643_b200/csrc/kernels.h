@@ -75,13 +75,14 @@ struct PlanBuffers {
   // tp > 1: the tp partial outputs of one item live part_stride uint4 apart (virtual
   // mode: the expert-output buffers of the slices; fused combine: the return buffers)
   long long part_stride;
-  // gather dispatch (P2P): every source's token block lands in tok [G][tok_rows][H] of every
-  // peer (copy engines); the source writes, for each of its rows a peer receives, the token
-  // buffer row into that peer's xmap [cap_rows]; the peer's k_expand copies the rows
+  // gather dispatch (P2P): every token row lands once in tok [G][tok_rows][H] of every peer
+  // hosting one of its experts; the source writes, for each of its rows a peer receives, the
+  // token-buffer row into that peer's xmap [cap_rows]; the peer's k_expand copies the rows
   uint4* recv_local;              // this rank's receive buffer
   const uint4* tok_local;         // this rank's token buffer
   const int32_t* xmap_local;      // this rank's row -> token-buffer row map
   int32_t* const* xmap_table;     // [G] every rank's xmap
+  uint4* const* tok_table;        // [G] every rank's token buffer
   unsigned* exp_counter;          // [G] k_expand last-CTA detection per source
   long long tok_rows;             // token-buffer rows per source (max_tokens)
   const int32_t* seg_meta_c;      // segment table (nseg at [0]) for k_expand

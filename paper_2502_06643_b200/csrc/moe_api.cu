@@ -115,14 +115,19 @@ struct moe_ctx {
   // 6.59 (128) in one run (profiles/r1_v13_timeline_ctas_*); Mixtral 4EP unchanged.
   // MOE_SCATTER_CTAS overrides.
   int remote_ctas = 32;
-  // gather dispatch (P2P): with top-k >= G/tp most tokens reach most
-  // ranks, so every token block is copied once to every peer by the copy engines
-  // (no SM time, host-known sizes), only a 4-byte row -> token index crosses per
-  // routed row, and the receiver expands its rows locally (k_expand).  Default for
-  // k >= G / tp; MOE_DISPATCH=scatter|gather overrides.
+  // gather dispatch (P2P): with top-k >= G/tp a token usually has
+  // several experts on one rank, so each token row crosses NVLink once per
+  // destination rank (not once per routed row), with a 4-byte row -> token index
+  // per routed row, and the receiver expands its rows locally (k_expand).  Opt-in
+  // (MOE_DISPATCH=gather): at E64 top-8 on 4 GPUs it halves the NVLink bytes, but
+  // the receiver's expansion costs more SM time next to K5 than the push saves
+  // (DESIGN.md §11).  (Copy-engine block
+  // copies were tried first: one peer cudaMemcpyAsync moves ~90 GB/s on this
+  // machine, profiles/r2_ce_probe.json -- far below the SMs' NVLink stores.)
   uint16_t* tokbuf = nullptr;           // [G][max_tokens][H]: every source's token block
   int32_t* xmap = nullptr;              // [cap_rows]: receive row -> token-buffer row
   int32_t** xmap_table = nullptr;       // device [G]
+  void** tok_table = nullptr;           // device [G]
   unsigned* exp_counter = nullptr;      // [G]
   std::vector<void*> tok_peer;          // host [G]: every rank's token buffer (peer pointers)
   bool last_gather = false;             // the last dispatch used the gather path
@@ -219,6 +224,7 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.tok_local = reinterpret_cast<const uint4*>(c->tokbuf);
   b.xmap_local = c->xmap;
   b.xmap_table = c->xmap_table;
+  b.tok_table = reinterpret_cast<uint4* const*>(c->tok_table);
   b.exp_counter = c->exp_counter;
   b.tok_rows = c->cfg.max_tokens;
   b.seg_meta_c = c->seg_meta;
@@ -513,6 +519,7 @@ static moe_status p2p_streams(moe_ctx_t ctx) {
   CU(cudaMalloc((void**)&ctx->tokbuf, tok_bytes));
   CU(cudaMalloc((void**)&ctx->xmap, sizeof(int32_t) * (size_t)ctx->cap_rows));
   CU(cudaMalloc((void**)&ctx->xmap_table, sizeof(void*) * (size_t)ctx->G));
+  CU(cudaMalloc((void**)&ctx->tok_table, sizeof(void*) * (size_t)ctx->G));
   CU(cudaMalloc((void**)&ctx->exp_counter, sizeof(unsigned) * (size_t)ctx->G));
   CU(cudaMemset(ctx->exp_counter, 0, sizeof(unsigned) * (size_t)ctx->G));
   ctx->tok_peer.assign(ctx->G, nullptr);
@@ -633,7 +640,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
     fail(ctx, MOE_ERR_CUDA, "descriptor table upload failed");
     return bail(MOE_ERR_CUDA);
   }
-  if (ctx->p2p && cudaMemcpy(ctx->xmap_table, xm.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess) {
+  if (ctx->p2p && (cudaMemcpy(ctx->xmap_table, xm.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) != cudaSuccess ||
+                   cudaMemcpy(ctx->tok_table, ctx->tok_peer.data(), sizeof(void*) * G, cudaMemcpyHostToDevice) !=
+                       cudaSuccess)) {
     fail(ctx, MOE_ERR_CUDA, "xmap table upload failed");
     return bail(MOE_ERR_CUDA);
   }
@@ -712,6 +721,7 @@ moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t*
     }
     cudaSetDevice(c->cfg.device);
     if (cudaMemcpy(c->xmap_table, xm.data(), sizeof(void*) * n, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(c->tok_table, c->tok_peer.data(), sizeof(void*) * n, cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy(c->desc_table, dsc.data(), sizeof(void*) * n, cudaMemcpyHostToDevice) != cudaSuccess) {
       fail(c, MOE_ERR_CUDA, "xmap table upload failed");
       return bail(MOE_ERR_CUDA, c);
@@ -759,7 +769,7 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
                  ctx->sendbuf, ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig,
                  ctx->sig, ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
                  ctx->epoch_dev, ctx->splitk_ws, ctx->tokbuf, ctx->xmap, ctx->xmap_table, ctx->exp_counter,
-                 ctx->desc, ctx->desc_table};
+                 ctx->desc, ctx->desc_table, ctx->tok_table};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -900,24 +910,11 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
     ctx->cur_join = ev_join;
   }
   // gather dispatch (see moe_ctx::tokbuf): top-k >= G/tp, or MOE_DISPATCH
-  bool gather = ctx->p2p && k >= n_grp;
+  bool gather = false;  // measured slower than scatter at E64 top-8 4EP: opt-in
   if (const char* dm = getenv("MOE_DISPATCH")) gather = ctx->p2p && !strcmp(dm, "gather");
   if (direct) gather = false;
   ctx->last_gather = gather;
   ctx->last_direct = direct;
-  if (gather && T > 0) {
-    // this rank's token block goes to every peer's token buffer (region `me`) on the
-    // copy engines, overlapping the plan kernels.  Safe to overwrite: every peer read
-    // the previous layer's block before raising the flag_y this rank's last combine
-    // waited for.
-    CU(cudaEventRecord(ev_fork, s));
-    CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-    const size_t bytes = (size_t)T * H * 2;
-    for (int g = 0; g < G; ++g)
-      if (g != ctx->me)
-        CU(cudaMemcpyAsync(static_cast<uint16_t*>(ctx->tok_peer[g]) + (size_t)ctx->me * ctx->cfg.max_tokens * H, x,
-                           bytes, cudaMemcpyDeviceToDevice, ctx->side));
-  }
   PlanArgs a = plan_args(ctx, T, k);
   a.gather = gather ? 1 : 0;
   a.direct = direct ? 1 : 0;
@@ -979,6 +976,10 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
     launch_expand_direct(a, b, ctx->remote_ctas, ctx->side);
     tl_rec(ctx, 3, ctx->side);
     CU(cudaEventRecord(ev_join, ctx->side));
+    // every receive row -- this rank's own tokens' too -- comes out of the expansion,
+    // and the plan arrays come from the side stream's descriptor kernel: join now
+    // (K5 has nothing to start on before the expansion anyway)
+    CU(cudaStreamWaitEvent(s, ev_join, 0));
     tl_rec(ctx, 2, s);
     LAUNCHED(ctx, 2);
   } else if (ctx->p2p) {
@@ -987,10 +988,12 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
     CU(cudaEventRecord(ev_fork, s));
     CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
     if (gather) {
-      // side stream: the row -> token-row map entries of the peers' rows (raising
-      // flag_data after the block copies above), then this rank's expansion of the
-      // rows its peers sent, source by source as they arrive
-      launch_scatter(a, x, idx, b, 5, ctx->side);
+      // side stream: each token row once to every rank hosting one of its experts,
+      // plus the row -> token-row map entries (flag_data), then this rank's expansion
+      // of the rows its peers sent, source by source as they arrive.  (Reusing the
+      // peers' token buffers is safe: every peer expanded the previous layer's rows
+      // before raising the flag_y this rank's last combine waited for.)
+      launch_scatter(a, x, idx, b, 5, ctx->side, ctx->remote_ctas);
       launch_expand(a, b, ctx->remote_ctas, ctx->side);
       LAUNCHED(ctx, 1);
     } else {

@@ -351,11 +351,13 @@ def test_group_detects_mismatched_placements(cuda_ok):
     g.close()
 
 
+@pytest.mark.parametrize("dispatch", ["scatter", "gather"])
 @pytest.mark.parametrize("G", [2, 4])
-def test_group_topk_at_least_ranks_default_gather(cuda_ok, G):
-    """The D5 regime (top-k >= EP ranks: E16 top-4 here, E64 top-8 in the bench)
-    takes the gather dispatch by default; uneven experts per rank (G14); plan,
-    payload, layer vs virtual ranks and the oracle."""
+def test_group_topk_at_least_ranks(cuda_ok, G, dispatch, monkeypatch):
+    """The D5 regime (top-k >= EP ranks: E16 top-4 here, E64 top-8 in the bench),
+    where the gather dispatch sends a token once per destination rank; uneven
+    experts per rank (G14); plan, payload, layer vs virtual ranks and the oracle."""
+    monkeypatch.setenv("MOE_DISPATCH", dispatch)
     moe = _moe()
     T, H, F, E, k = 900, 128, 256, 16, 4
     P = np.array([(3 * e + e // 5) % G for e in range(E)])

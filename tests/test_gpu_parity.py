@@ -492,6 +492,7 @@ def _chain_home_and_direct(make, inp_list, plans, k, E, dev_ws):
         home.expert_ffn(w13, w2)
         x = home.combine(w)
     home.sync()
+    home_out = x
     ctxs = [make(), make()]
     x = x0
     prev = prev_w = None
@@ -507,7 +508,7 @@ def _chain_home_and_direct(make, inp_list, plans, k, E, dev_ws):
         prev, prev_w = c, w
     out = prev.combine(prev_w)
     prev.sync()
-    return x, out
+    return home_out, out
 
 
 @pytest.mark.parametrize("G", [1, 4])

@@ -70,14 +70,19 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    uid = None
-    if N > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    def fresh_uid():
+        """A new NCCL unique id for each context (one communicator per context)."""
+        if N == 1:
+            return None
         u = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
             u.copy_(torch.frombuffer(bytearray(moe.get_unique_id()), dtype=torch.uint8))
         dist.broadcast(u, 0)
-        uid = bytes(u.cpu().numpy().tobytes())
+        return bytes(u.cpu().numpy().tobytes())
+
+    if N > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    uid = fresh_uid()
     t0, t1 = blocks(T, N)[rank]
     Tmax = max(y - x for x, y in blocks(T, N))
     lay = moe.MoeLayer(max_tokens=max(Tmax, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N, rank=rank,
@@ -161,7 +166,7 @@ def main():
     dl = []
     if a.direct:
         dl = [moe.MoeLayer(max_tokens=max(Tmax, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N, rank=rank,
-                           device=local, uid=uid, a2a="p2p" if N > 1 else "nccl") for _ in range(2)]
+                           device=local, uid=fresh_uid(), a2a="p2p" if N > 1 else "nccl") for _ in range(2)]
         for c in dl:
             for name, plan in plans.items():
                 for li in range(L):
