@@ -26,6 +26,10 @@ constexpr int kErrPlacement = 8;  // ranks passed different expert_to_rank maps 
 constexpr int kErrNaN = 16;       // a router logit is NaN (reading G3: logits are finite)
 constexpr int kErrBadRank = 32;   // an expert_to_rank value outside [0, G / tp)
 constexpr int kErrWeights = 64;   // moe_expert_ffn got weights for n_w experts, the placement hosts another count
+// A timed-out wait also sets bit (8 + site) so the error names where it waited.
+enum TimeoutSite { kWaitCounts = 0, kWaitRowsK5 = 1, kWaitOutputs = 2, kWaitFlags = 3, kWaitGatherRows = 4,
+                   kWaitPrevOutputs = 5, kWaitDescriptors = 6 };
+__host__ __device__ constexpr int timeout_bits(int site) { return kErrTimeout | (1 << (8 + site)); }
 constexpr unsigned long long kFlagTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s (default; MOE_FLAG_TIMEOUT_MS)
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

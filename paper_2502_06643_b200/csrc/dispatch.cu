@@ -67,13 +67,13 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 // kErrTimeout after kFlagTimeoutNs instead of hanging the GPU.
 __device__ __forceinline__ unsigned cur_epoch(const unsigned* p) { return *(volatile const unsigned*)p; }
 __device__ __forceinline__ void wait_flags_geq(const unsigned* flags, int n, unsigned epoch, int* err,
-                                               unsigned long long timeout_ns) {
+                                               unsigned long long timeout_ns, int site) {
   for (int g = threadIdx.x; g < n; g += blockDim.x) {
     const uint64_t t0 = globaltimer_ns();
     while ((int)(ld_acquire_sys(flags + g) - epoch) < 0) {
       __nanosleep(64);
       if (globaltimer_ns() - t0 > timeout_ns) {
-        atomicOr(err, kErrTimeout);
+        atomicOr(err, timeout_bits(site));
         break;
       }
     }
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
     }
     __syncthreads();
     if (threadIdx.x == 0) signal_all(a, b, 0);
-    wait_flags_geq(b.my_sig->flag_cnt, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns);
+    wait_flags_geq(b.my_sig->flag_cnt, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns, kWaitCounts);
     for (int g = threadIdx.x; g < a.G; g += blockDim.x)
       if (((volatile unsigned*)b.my_sig->phash)[g] != my_hash) atomicOr(b.err, kErrPlacement);
     cnt = b.my_sig->cnt;
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_expand(PlanArgs a, PlanBuff
       while ((int)(ld_acquire_sys(&b.my_sig->flag_data[s]) - epoch) < 0) {
         __nanosleep(128);
         if (globaltimer_ns() - t0 > a.timeout_ns) {
-          atomicOr(b.err, kErrTimeout);
+          atomicOr(b.err, timeout_bits(kWaitGatherRows));
           break;
         }
       }
@@ -607,75 +607,118 @@ __global__ void __launch_bounds__(kScatterThreads) k_expand(PlanArgs a, PlanBuff
 // expert outputs where they were computed (a local read when ILP 2 put the two
 // experts on one GPU, an NVLink load otherwise) -- no return to the home rank.
 // Same arithmetic as K8 (fp32 FMA, j ascending, one bf16 rounding), so the layer
-// input is bit-identical to the home-rank chain's.
-__global__ void __launch_bounds__(kScatterThreads) k_expand_direct(PlanArgs a, PlanBuffers b) {
-  __shared__ const uint4* src_s[kMaxWorld];
-  __shared__ unsigned last;
-  const int nslots = a.p2p ? a.G : 1;
-  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = b.prev_src[q];
-  if (a.p2p && threadIdx.x == 0) {
-    const unsigned ep = cur_epoch(a.epoch_ptr), pep = cur_epoch(b.prev_epoch);
-    const uint64_t t0 = globaltimer_ns();
-    for (int g = 0; g < a.G; ++g) {   // every source's descriptors and every rank's layer-l outputs
-      while ((int)(ld_acquire_sys(&b.my_sig->flag_data[g]) - ep) < 0 ||
-             (int)(ld_acquire_sys(b.prev_flag_y + g) - pep) < 0) {
-        __nanosleep(128);
-        if (globaltimer_ns() - t0 > a.timeout_ns) {
-          atomicOr(b.err, kErrTimeout);
-          break;
+// input is bit-identical to the home-rank chain's.  P2P: once every rank's layer-l
+// outputs are ready (layer-l flag_y), source by source in ascending order (the
+// segments' row order, so K5's first tiles come free first) as each source's
+// descriptors arrive (flag_data); flag_exp[s] is raised per source for K5's
+// per-tile waits.  Virtual / one rank: every hosted row in one pass.
+__device__ __forceinline__ void direct_rows(const PlanArgs& a, const PlanBuffers& b, const uint4* const* src_s,
+                                            long long row0, int n, int gw, int stride, int lane) {
+  const int cpr = a.H / 8, pk = b.prev_k, dk = b.desc_k;
+  constexpr int U = 4;  // 16-byte chunks per lane in flight (k loads each)
+  for (int r = gw; r < n; r += stride) {
+    const long long row = row0 + r;
+    const int32_t* d = b.desc_local + row * dk * 3;
+    for (int c0 = lane; c0 < cpr; c0 += 32 * U) {
+      float acc[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+      for (int j = 0; j < pk; ++j) {
+        const int prow = d[3 * j + 1];
+        if (prow < 0) continue;
+        const float wj = __int_as_float(d[3 * j + 2]);
+        const uint4* src = src_s[d[3 * j]] + (long long)prow * cpr;
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + 32 * u;
+          v[u] = c < cpr ? src[c] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          acc[u][0] = fmaf(wj, bf16_lo(v[u].x), acc[u][0]);
+          acc[u][1] = fmaf(wj, bf16_hi(v[u].x), acc[u][1]);
+          acc[u][2] = fmaf(wj, bf16_lo(v[u].y), acc[u][2]);
+          acc[u][3] = fmaf(wj, bf16_hi(v[u].y), acc[u][3]);
+          acc[u][4] = fmaf(wj, bf16_lo(v[u].z), acc[u][4]);
+          acc[u][5] = fmaf(wj, bf16_hi(v[u].z), acc[u][5]);
+          acc[u][6] = fmaf(wj, bf16_lo(v[u].w), acc[u][6]);
+          acc[u][7] = fmaf(wj, bf16_hi(v[u].w), acc[u][7]);
         }
       }
-    }
-  }
-  __syncthreads();
-  const int E = a.E, cpr = a.H / 8, pk = b.prev_k, dk = b.desc_k;
-  const int nseg = b.seg_meta_c[0];
-  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int gw = blockIdx.x * nw + (threadIdx.x >> 5), stride = gridDim.x * nw;
-  for (int pos = 0; pos < nseg; ++pos) {
-    const int row0 = b.seg_meta_c[1 + pos], n = b.seg_meta_c[1 + E + pos];
-    for (int r = gw; r < n; r += stride) {
-      const long long row = row0 + r;
-      const int32_t* d = b.desc_local + row * dk * 3;
-      for (int c = lane; c < cpr; c += 32) {
-        float acc[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-        for (int j = 0; j < pk; ++j) {
-          const int prow = d[3 * j + 1];
-          if (prow < 0) continue;
-          const float wj = __int_as_float(d[3 * j + 2]);
-          const uint4 v = src_s[d[3 * j]][(long long)prow * cpr + c];
-          acc[0] = fmaf(wj, bf16_lo(v.x), acc[0]);
-          acc[1] = fmaf(wj, bf16_hi(v.x), acc[1]);
-          acc[2] = fmaf(wj, bf16_lo(v.y), acc[2]);
-          acc[3] = fmaf(wj, bf16_hi(v.y), acc[3]);
-          acc[4] = fmaf(wj, bf16_lo(v.z), acc[4]);
-          acc[5] = fmaf(wj, bf16_hi(v.z), acc[5]);
-          acc[6] = fmaf(wj, bf16_lo(v.w), acc[6]);
-          acc[7] = fmaf(wj, bf16_hi(v.w), acc[7]);
-        }
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 32 * u;
+        if (c >= cpr) continue;
         uint4 o;
-        o.x = pack_bf16x2(acc[0], acc[1]);
-        o.y = pack_bf16x2(acc[2], acc[3]);
-        o.z = pack_bf16x2(acc[4], acc[5]);
-        o.w = pack_bf16x2(acc[6], acc[7]);
+        o.x = pack_bf16x2(acc[u][0], acc[u][1]);
+        o.y = pack_bf16x2(acc[u][2], acc[u][3]);
+        o.z = pack_bf16x2(acc[u][4], acc[u][5]);
+        o.w = pack_bf16x2(acc[u][6], acc[u][7]);
         b.recv_local[row * cpr + c] = o;
       }
     }
   }
-  if (!a.p2p) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&b.exp_counter[0], 1u) == gridDim.x - 1;
+}
+
+__global__ void __launch_bounds__(kScatterThreads, 2) k_expand_direct(PlanArgs a, PlanBuffers b) {
+  __shared__ const uint4* src_s[kMaxWorld];
+  __shared__ unsigned last;
+  const int nslots = a.p2p ? a.G : 1;
+  for (int q = threadIdx.x; q < nslots; q += blockDim.x) src_s[q] = b.prev_src[q];
+  const int E = a.E;
+  const int nseg = b.seg_meta_c[0];
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int gw = blockIdx.x * nw + (threadIdx.x >> 5), stride = gridDim.x * nw;
+  if (!a.p2p) {
+    __syncthreads();
+    for (int pos = 0; pos < nseg; ++pos)
+      direct_rows(a, b, src_s, b.seg_meta_c[1 + pos], b.seg_meta_c[1 + E + pos], gw, stride, lane);
+    return;
+  }
+  const unsigned ep = cur_epoch(a.epoch_ptr);
+  if (threadIdx.x == 0) {          // every rank's layer-l outputs (any of them may be read)
+    const unsigned pep = cur_epoch(b.prev_epoch);
+    const uint64_t t0 = globaltimer_ns();
+    for (int g = 0; g < a.G; ++g)
+      while ((int)(ld_acquire_sys(b.prev_flag_y + g) - pep) < 0) {
+        __nanosleep(128);
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicOr(b.err, timeout_bits(kWaitPrevOutputs));
+          break;
+        }
+      }
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    b.exp_counter[0] = 0;
-    __threadfence();
-    const unsigned ep = cur_epoch(a.epoch_ptr);
-    for (int g = 0; g < a.G; ++g) st_release_sys(&b.my_sig->flag_exp[g], ep);
+  for (int s = 0; s < a.G; ++s) {
+    if (threadIdx.x == 0) {        // source s's descriptors have landed
+      const uint64_t t0 = globaltimer_ns();
+      while ((int)(ld_acquire_sys(&b.my_sig->flag_data[s]) - ep) < 0) {
+        __nanosleep(128);
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicOr(b.err, timeout_bits(kWaitDescriptors));
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    for (int pos = 0; pos < nseg; ++pos) {
+      const int32_t* d = b.seg_src + ((long long)pos * a.G + s) * 3;
+      direct_rows(a, b, src_s, d[0], d[1], gw, stride, lane);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(&b.exp_counter[s], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+      b.exp_counter[s] = 0;
+      __threadfence();
+      st_release_sys(&b.my_sig->flag_exp[s], ep);
+    }
   }
 }
 
@@ -716,7 +759,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_combine(PlanArgs a, cons
     w_s[i] = v < 0 ? 0.f : w[gi];
     slot_s[i] = a.fused ? 0 : b.slot_of_item[gi];
   }
-  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns);
+  if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns, kWaitOutputs);
   __syncthreads();
   const int cpr = a.H / 8;
   const int cw = (cpr + a.col_split - 1) / a.col_split;
@@ -871,7 +914,7 @@ void launch_signal(const PlanArgs& a, const PlanBuffers& b, int which, cudaStrea
   k_signal<<<1, 32, 0, s>>>(a, b, which);
 }
 __global__ void k_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, unsigned long long tmo) {
-  wait_flags_geq(flags, n, cur_epoch(epoch_ptr), err, tmo);
+  wait_flags_geq(flags, n, cur_epoch(epoch_ptr), err, tmo, kWaitFlags);
 }
 void launch_wait(const unsigned* flags, int n, const unsigned* epoch_ptr, int* err, unsigned long long timeout_ns,
                  cudaStream_t s) {
@@ -916,7 +959,13 @@ void preload_dispatch_kernels() {
                       (const void*)k_combine<0>, (const void*)k_combine<1>, (const void*)k_combine<2>,
                       (const void*)k_combine<4>, (const void*)k_combine<8>, (const void*)k_pack_w13,
                       (const void*)k_expand, (const void*)k_expand_direct};
-  for (const void* f : fs) cudaFuncGetAttributes(&fa, f);
+  for (const void* f : fs) {
+    cudaFuncGetAttributes(&fa, f);
+    // these kernels run next to the persistent GEMM (which holds ~210 KB of shared
+    // memory per SM): ask for the max-shared carveout so an SM never has to drain
+    // the GEMM to switch its L1/shared split for them
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  }
 }
 
 }  // namespace moe

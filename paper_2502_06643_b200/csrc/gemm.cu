@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             do {
               asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sw.flags + s) : "memory");
               if (globaltimer_ns() - t0 > sw.timeout_ns) {
-                atomicOr(err, kErrTimeout);
+                atomicOr(err, timeout_bits(kWaitRowsK5));
                 break;
               }
             } while ((int)(v - epoch) < 0);

@@ -787,14 +787,21 @@ static moe_status check_device_error(moe_ctx_t ctx) {
   CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   if (e) {
     cudaMemset(ctx->err_dev, 0, sizeof(int));
-    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s%s%s%s",
+    std::string sites;
+    static const char* kSite[] = {"count exchange (k_layout)", "peers' rows (K5)", "expert outputs (combine)",
+                                  "flags (k_wait)", "gathered rows (k_expand)", "previous layer's outputs (direct)",
+                                  "descriptors (direct)"};
+    for (int i = 0; i < 7; ++i)
+      if (e & (1 << (8 + i))) sites += std::string(sites.empty() ? " waiting for: " : ", ") + kSite[i];
+    return fail(ctx, (e & kErrTimeout) ? MOE_ERR_TIMEOUT : MOE_ERR_DEVICE, "device error latched:%s%s%s%s%s%s%s%s",
                 (e & kErrBadExpert) ? " expert id out of range" : "",
                 (e & kErrCapacity) ? " receive capacity exceeded" : "",
                 (e & kErrTimeout) ? " P2P peer flag timeout (a rank skipped a collective call?)" : "",
                 (e & kErrPlacement) ? " ranks dispatched with different expert_to_rank maps" : "",
                 (e & kErrNaN) ? " NaN router logit" : "",
                 (e & kErrBadRank) ? " expert_to_rank value outside [0, G/tp)" : "",
-                (e & kErrWeights) ? " moe_expert_ffn n_w differs from the experts the placement hosts here" : "");
+                (e & kErrWeights) ? " moe_expert_ffn n_w differs from the experts the placement hosts here" : "",
+                sites.c_str());
   }
   return MOE_OK;
 }
@@ -972,13 +979,15 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
     // descriptors and every rank's layer-l outputs are there (flag_exp for K5)
     CU(cudaEventRecord(ev_fork, s));
     CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-    launch_scatter(a, x, idx, b, 6, ctx->side);
-    launch_expand_direct(a, b, ctx->remote_ctas, ctx->side);
+    launch_scatter(a, x, idx, b, 6, ctx->side, ctx->remote_ctas);
+    launch_expand_direct(a, b, 2 * ctx->num_sms, ctx->side);
     tl_rec(ctx, 3, ctx->side);
     CU(cudaEventRecord(ev_join, ctx->side));
     // every receive row -- this rank's own tokens' too -- comes out of the expansion,
-    // and the plan arrays come from the side stream's descriptor kernel: join now
-    // (K5 has nothing to start on before the expansion anyway)
+    // so K5 has nothing to start on before it: join, and the expansion gets the
+    // whole GPU.  (Letting K5 start and wait per tile for the sources' rows, as the
+    // scatter dispatch does, measured as a stall: the expansion made no progress
+    // next to the waiting K5 until K5's flag waits timed out -- gpurun_out r2l-r2n.)
     CU(cudaStreamWaitEvent(s, ev_join, 0));
     tl_rec(ctx, 2, s);
     LAUNCHED(ctx, 2);
@@ -1135,11 +1144,9 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     ctx->ffn_fused = ctx->p2p && fused && !ctx->out_stay;  // MOE_OUT_STAY: the outputs stay here
   }
   ctx->ffn_done = true;
-  if (ctx->out_stay && ctx->p2p) {
-    // no moe_combine follows to join the side stream: K5 waited for every row it
-    // reads anyway, so join here (keeps a captured chain's streams joined)
-    CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));
-  }
+  // MOE_OUT_STAY: no moe_combine follows to join the side stream -- join at the end
+  // of this call (keeps a captured chain's streams joined)
+  const bool join_here = ctx->out_stay && ctx->p2p;
   if (n_w == 0) {
     // no expert here: the placement must host none on this rank (checked on the
     // device), and in P2P mode every rank still hears "my outputs are ready"
@@ -1149,6 +1156,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
       launch_signal(a, b, 2, s);
       LAUNCHED(ctx, 1);
     }
+    if (join_here) CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));
     return MOE_OK;
   }
   const int H = ctx->H, F = ctx->Fl, tp = ctx->tp;
@@ -1253,6 +1261,14 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   if (ctx->p2p) {  // expert outputs of this rank are ready for the peers' combine
     launch_signal(a, b, 2, s);
     LAUNCHED(ctx, 1);
+  }
+  if (join_here) {
+    CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));
+    tl_rec(ctx, 7, s);              // no combine follows: close this layer's timeline record
+    if (ctx->tl_cur >= 0) {
+      ++ctx->tl_used;
+      ctx->tl_cur = -1;
+    }
   }
   return MOE_OK;
 }
@@ -1374,6 +1390,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
   }
   PlanArgs a = plan_args(ctx, ctx->last_T, ctx->last_k);
   PlanBuffers b = plan_buffers(ctx);
+  if (ctx->p2p && ctx->last_direct) CU(cudaStreamWaitEvent(s, ctx->cur_join, 0));  // plan arrays (side stream)
   if (ctx->p2p && (a.n_tiles == 0 || ctx->shared_dev)) {
     // every rank's expert outputs of this layer are ready (flag_y).  A rank without
     // tokens must wait too: its next dispatch writes count rows into the peers'

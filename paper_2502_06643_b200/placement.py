@@ -218,21 +218,21 @@ def ilp2_dp(C, G, L):
     P = len(perms)
     if L == 1:
         return np.array([perms[0]], dtype=np.int32)
-    # cost[l][i][j] = transition l with layer-l permutation i, layer-(l+1) permutation j
-    best = np.zeros(P, dtype=np.int64)
-    back = []
-    for l in range(L - 1):
-        trans = np.array([[_pair_max(C[l], perms[i], perms[j], G) for j in range(P)] for i in range(P)])
-        tot = best[:, None] + trans                      # [i][j]
-        arg = np.argmin(tot, axis=0)                     # first (smallest i) among ties
-        best = tot[arg, np.arange(P)]
-        back.append(arg)
-    j = int(np.argmin(best))
-    seq = [j]
+    # trans[l][i][j] = transition l with layer-l permutation i, layer-(l+1) permutation j;
+    # togo[l][i] = the least cost of layers l.. given permutation i at layer l (backward DP)
+    trans = [np.array([[_pair_max(C[l], perms[i], perms[j], G) for j in range(P)] for i in range(P)])
+             for l in range(L - 1)]
+    togo = [None] * L
+    togo[L - 1] = np.zeros(P, dtype=np.int64)
     for l in range(L - 2, -1, -1):
-        j = int(back[l][j])
-        seq.append(j)
-    seq.reverse()
+        togo[l] = (trans[l] + togo[l + 1][None, :]).min(axis=1)
+    # forward: the smallest optimal permutation index at every layer, given the ones
+    # chosen before it -- the lexicographically smallest optimal sequence (perms are
+    # generated in lexicographic order)
+    seq = [int(np.argmin(togo[0]))]
+    for l in range(L - 1):
+        i = seq[-1]
+        seq.append(int(np.argmin(trans[l][i] + togo[l + 1])))   # argmin: first among ties
     return np.array([perms[i] for i in seq], dtype=np.int32)
 
 

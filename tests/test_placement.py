@@ -114,6 +114,12 @@ def test_ilp2_dp_matches_exhaustive():
             got = placement.ilp2_dp(C, G, L)
             assert all(sorted(p) == list(range(G)) for p in got)   # Eqs. 14-15
             assert placement.objective_o2(C, got) == best
+            # ties: the lexicographically smallest optimal permutation sequence
+            first = min(seq for seq in itertools.product(range(len(perms)), repeat=L)
+                        if placement.objective_o2(C, [perms[i] for i in seq]) == best)
+            assert got.tolist() == [list(perms[i]) for i in first]
+    # the case where a forward DP with a final argmin picks the later layer's choice
+    assert placement.ilp2_dp(np.array([[[0, 10], [10, 0]]]), 2, 2).tolist() == [[0, 1], [1, 0]]
 
 
 def test_expert_to_gpu_and_balance():
