@@ -314,10 +314,12 @@ def test_mixtral_layer_full_size_every_tile(cuda_ok, G, P, s):
     lay.close()
 
 
-def test_e64_layer_full_size_sampled(cuda_ok):
+def test_e64_layer_full_size_every_tile(cuda_ok):
     """BASELINE configs[4] shape (E64 top-8, H4096, F2048, T = 65536) over 4
-    virtual EP ranks with the ILP-1 balanced placement, checked on sampled tokens
-    against the oracle's direct definition (each sampled token touches 8 experts)."""
+    virtual EP ranks with the ILP-1 balanced placement, checked against the
+    oracle's direct definition on tokens chosen so that every 256-row M tile of
+    every expert segment holds a checked row (tile_cover_tokens; each token
+    touches 8 experts)."""
     from paper_2502_06643_b200 import placement
     T, H, F, E, k, G = 65536, 4096, 2048, 64, 8, 4
     dev = torch.device(DEV)
@@ -335,7 +337,7 @@ def test_e64_layer_full_size_sampled(cuda_ok):
     lay.expert_ffn(w13, w2)
     out = lay.combine(w)
     lay.sync()
-    sel = np.array(sorted(set(np.random.default_rng(1).integers(0, T, 40).tolist()) | {0, T - 1}))
+    sel = tile_cover_tokens(idx.cpu().numpy(), E, 256, seed=5)
     xs = bf16_to_f64(x[sel])
     ls = logits[sel].cpu().numpy()
     cache = {}
