@@ -69,6 +69,19 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, uint32_t ssrc, uint32_t byt
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// shared::cta -> global bulk copy with an L2 cache policy (e.g. evict-first for rows the
+// destination will not re-read soon)
+__device__ __forceinline__ void bulk_s2g_hint(void* gdst, uint32_t ssrc, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(ssrc), "r"(bytes), "l"(policy)
+               : "memory");
+}
+// global -> shared::cta bulk copy whose completion is signalled on an mbarrier of this CTA
+__device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void* gsrc, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(bar)
+               : "memory");
+}
 // L2 policy for streamed outputs: evict first (a GEMM's output is read back only by
 // the next kernel, after far more than L2's worth of other traffic; keeping it out of
 // the way keeps the operand tiles of the rasterisation group resident)

@@ -412,7 +412,12 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   // the plan arrays (row / slot / send slot of every item) come from the launch that
   // covers this rank's items on the caller's stream: modes 0 and 1, or -- direct
   // dispatch, which copies no rows -- mode 6
-  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt, part == 0 && (mode == 0 || mode == 1 || mode == 6));
+  tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt,
+             part == 0 && (mode == 0 || (mode == 1 && !a.plan_done) || mode == 3 || mode == 6));
+  if (mode == 3) {  // plan arrays only
+    __syncthreads();
+    continue;
+  }
   if (mode == 6) {
     // direct dispatch: instead of x rows, every destination row gets the locations and
     // gate weights of the k layer-l expert outputs it combines
@@ -536,7 +541,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   }
   __syncthreads();  // it / run are reused by the next work unit
   }
-  if (a.p2p && (mode == 0 || mode == 2 || mode == 5 || mode == 6)) {
+  if (a.p2p && (mode == 0 || mode == 5 || mode == 6)) {
     // the last CTA to finish raises flag_data[me] on every rank
     __threadfence_system();
     __syncthreads();
@@ -547,6 +552,120 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
       signal_all(a, b, 1);
     }
   }
+}
+
+__global__ void k_signal(PlanArgs a, PlanBuffers b, int which);
+
+// ----------------------------------------------------------------- TMA push of the peers' rows
+// The dispatch of the rows this rank sends to its peers (P2P; K3's remote half).
+// One warp per CTA, tokens in batches of 32 (one per lane): each lane collects its
+// token's remote destinations (receive rows on peers; tp > 1: every rank of the
+// item's group but this one) into shared memory; then lane 0 drives the bulk-copy
+// (TMA) engine over the batch's (token, 4 KB piece) units -- one global -> shared
+// copy of the piece, one shared -> global copy into every remote receive row, with
+// an L2 evict-first hint (the destination reads it only when its GEMM gets there)
+// -- with two pieces in flight.  Almost no SM instructions, so the grid (one CTA
+// per SM, ~12 KB of shared memory) interferes little with the expert GEMM it runs
+// next to: measured against 32 CTAs of 16-byte SM stores (the round-1 design),
+// −4% per layer at Mixtral 4EP balanced, −1-2% at E64 top-8 4EP
+// (profiles/r2_timeline_push_*).
+constexpr int kPushStages = 2;
+constexpr int kPushPiece = 4096;
+constexpr int kPushDest = kMaxK * kMaxTP;  // destinations per token (k items x tp ranks)
+__global__ void __launch_bounds__(32) k_push_tma(PlanArgs a, const uint8_t* __restrict__ x, PlanBuffers b) {
+  __shared__ alignas(128) uint8_t stage_s[kPushStages][kPushPiece];
+  __shared__ alignas(8) uint64_t full[kPushStages];
+  __shared__ int2 dst_s[32][kMaxK];   // (destination slot, receive row) per (token of the batch, item)
+  __shared__ int ndst_s[32];
+  const int lane = threadIdx.x;
+  const int rowb = a.H * 2;
+  const int piece = rowb % kPushPiece == 0 ? kPushPiece : rowb;  // rows <= 4 KB go whole
+  const int npieces = rowb / piece;
+  if (lane == 0) {
+    for (int q = 0; q < kPushStages; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase_bits = 0;  // bit q = phase of stage q
+  const uint64_t pol = l2_evict_first_policy();
+  const int nbatch = (a.T + 31) / 32;
+  for (int bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
+    const int t = bt * 32 + lane;
+    int nd = 0;
+    if (t < a.T) {
+      for (int j = 0; j < a.k; ++j) {
+        const long long gi = (long long)t * a.k + j;
+        const int row = b.row_of_item[gi], slot = b.slot_of_item[gi];
+        // tp > 1: the slot is an EP group whose every rank but this one gets the row
+        if (row >= 0 && (a.tp > 1 || slot != a.me)) dst_s[lane][nd++] = make_int2(slot, row);
+      }
+    }
+    ndst_s[lane] = nd;
+    __syncwarp();
+    if (lane == 0) {
+      // the batch's units (token l, piece pc) with ndst > 0, in order, through a ring of
+      // kPushStages shared-memory slots: up to kPushStages pieces loading at once
+      int l = 0, pc = 0;
+      while (l < 32 && ndst_s[l] == 0) ++l;
+      int lq[kPushStages], pq[kPushStages];
+      int issued = 0, done = 0;
+      while (true) {
+        while (issued - done < kPushStages && l < 32) {
+          const int q = issued % kPushStages;
+          lq[q] = l;
+          pq[q] = pc;
+          const uint32_t bar = smem_u32(&full[q]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(piece) : "memory");
+          bulk_g2s(smem_u32(stage_s[q]), x + (long long)(bt * 32 + l) * rowb + (long long)pc * piece, piece, bar);
+          ++issued;
+          if (++pc == npieces) {
+            pc = 0;
+            do ++l; while (l < 32 && ndst_s[l] == 0);
+          }
+        }
+        if (done == issued) break;
+        const int q = done % kPushStages;
+        mbar_wait(&full[q], (phase_bits >> q) & 1u);
+        phase_bits ^= 1u << q;
+        const int lt = lq[q];
+        const long long off = (long long)pq[q] * piece;
+        for (int d = 0; d < ndst_s[lt]; ++d) {
+          const int2 sr = dst_s[lt][d];
+          for (int tq = 0; tq < a.tp; ++tq) {
+            const int r = a.tp == 1 ? sr.x : sr.x * a.tp + tq;
+            if (r == a.me) continue;
+            bulk_s2g_hint(reinterpret_cast<uint8_t*>(b.dst_table[r]) + (long long)sr.y * rowb + off,
+                          smem_u32(stage_s[q]), piece, pol);
+          }
+        }
+        bulk_commit();
+        ++done;
+        // the slot is refilled next: its stores must have read it
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+    }
+    __syncwarp();
+  }
+  // every store complete and visible before the arrival flag
+  __shared__ unsigned last;
+  if (lane == 0) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();
+    last = atomicAdd(b.done_counter, 1u) == gridDim.x - 1;
+    if (last) {
+      *b.done_counter = 0;
+      signal_all(a, b, 1);
+    }
+  }
+}
+
+void launch_push_tma(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int ctas, cudaStream_t s) {
+  if (a.T <= 0) {
+    k_signal<<<1, 32, 0, s>>>(a, b, 1);
+    return;
+  }
+  k_push_tma<<<ctas, 32, 0, s>>>(a, reinterpret_cast<const uint8_t*>(x), b);
 }
 
 // ----------------------------------------------------------------- gather dispatch: expand
@@ -896,17 +1015,17 @@ void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cu
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
                     cudaStream_t s, int max_ctas) {
   const size_t smem = sizeof(int) * (kScatterThreads / 32) * a.E;
-  int grid = a.n_tiles * (mode == 6 ? 1 : a.col_split);
+  int grid = a.n_tiles * ((mode == 6 || mode == 3) ? 1 : a.col_split);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (a.n_tiles > 0) {
-    if (mode == 6) {  // one CTA per token tile (no column slices: no rows are copied)
+    if (mode == 6 || mode == 3) {  // one CTA per token tile (no column slices: no rows are copied)
       PlanArgs a1 = a;
       a1.col_split = 1;
       k_scatter<<<grid, kScatterThreads, smem, s>>>(a1, (const uint4*)x, idx, b, mode);
     } else {
       k_scatter<<<grid, kScatterThreads, smem, s>>>(a, (const uint4*)x, idx, b, mode);
     }
-  } else if (a.p2p && (mode == 0 || mode == 2 || mode == 5 || mode == 6)) {
+  } else if (a.p2p && (mode == 0 || mode == 5 || mode == 6)) {
     k_signal<<<1, 32, 0, s>>>(a, b, 1);
   }
 }
@@ -958,7 +1077,7 @@ void preload_dispatch_kernels() {
                       (const void*)k_signal, (const void*)k_wait, (const void*)k_expect_nseg,
                       (const void*)k_combine<0>, (const void*)k_combine<1>, (const void*)k_combine<2>,
                       (const void*)k_combine<4>, (const void*)k_combine<8>, (const void*)k_pack_w13,
-                      (const void*)k_expand, (const void*)k_expand_direct};
+                      (const void*)k_expand, (const void*)k_expand_direct, (const void*)k_push_tma};
   for (const void* f : fs) {
     cudaFuncGetAttributes(&fa, f);
     // these kernels run next to the persistent GEMM (which holds ~210 KB of shared

@@ -39,6 +39,7 @@ struct PlanArgs {
                              // (k_layout increments it, so captured CUDA graphs replay correctly)
   int n_tiles;  // sum over sources of ceil(T_s / kTileTokens)
   int col_split;  // K3/K8: CTAs per token tile, each copying a slice of the hidden dim
+  int plan_done;  // the plan arrays of this dispatch were written already (mode 3): mode 1 skips them
   int seg_align;  // expert segments are padded to this many rows (= the GEMM M tile, 128 or 256)
   int fused;      // K8 reads the local return buffer at the C3 slot (fused-combine mode)
   int gather;     // P2P gather dispatch: token rows reach the peers by copy engine, rows are
@@ -131,7 +132,8 @@ int plan_tiles(int T, int V);
 void launch_count(const PlanArgs& a, const int32_t* idx, const PlanBuffers& b, cudaStream_t s);
 void launch_scan(const PlanArgs& a, const PlanBuffers& b, cudaStream_t s);
 void launch_layout(const PlanArgs& a, const PlanBuffers& b, int64_t cap_rows, cudaStream_t s);
-// mode 0: all rows; P2P overlap: 1 = rows hosted here (+ plan arrays), 2 = rows for peers,
+// mode 0: all rows; P2P: 3 = the plan arrays only (before the TMA push of the peers' rows),
+// 1 = rows hosted here,
 // 5 = gather dispatch: only the row -> token-buffer map entries of the peers' rows,
 // 6 = direct dispatch: the combine descriptors of every row (all destinations, own included)
 void launch_scatter(const PlanArgs& a, const uint16_t* x, const int32_t* idx, const PlanBuffers& b, int mode,
@@ -141,6 +143,10 @@ void launch_combine(const PlanArgs& a, const float* w, const PlanBuffers& b, uin
 // ascending -- the home-rank combine's arithmetic); P2P: after every source's descriptors
 // (flag_data) and every rank's layer-l outputs (layer-l flag_y) arrived; raises flag_exp.
 void launch_expand_direct(const PlanArgs& a, const PlanBuffers& b, int max_ctas, cudaStream_t s);
+// P2P dispatch of the peers' rows on the TMA engines: one warp per CTA bulk-copies each
+// token row (in 4 KB pieces) from x into shared memory once and from there into every
+// remote receive row of its items; reads the plan arrays (mode 3); raises flag_data.
+void launch_push_tma(const PlanArgs& a, const uint16_t* x, const PlanBuffers& b, int ctas, cudaStream_t s);
 // Gather dispatch: expand every peer's token rows (token buffer -> receive layout),
 // source by source as each source's flag_data arrives; raises flag_exp per source.
 void launch_expand(const PlanArgs& a, const PlanBuffers& b, int max_ctas, cudaStream_t s);

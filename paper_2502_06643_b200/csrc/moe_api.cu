@@ -253,6 +253,7 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.fused = c->p2p && c->ffn_fused;
   a.gather = 0;
   a.direct = 0;
+  a.plan_done = 0;
   a.timeout_ns = c->flag_timeout_ns;
   // enough CTAs for the HBM/NVLink-bound row copies, but no partial second wave:
   // K3/K8 CTAs (512 threads) fit twice per SM, so aim at <= 2 x num_sms CTAs
@@ -994,9 +995,19 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
   } else if (ctx->p2p) {
     // rows for peers: NVLink stores on the side stream (arrival flags raised by its
     // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
+    if (!gather) {
+      // the plan arrays first (the TMA push reads them), then the fork
+      launch_scatter(a, x, idx, b, 3, s);
+      a.plan_done = 1;
+      LAUNCHED(ctx, 1);
+    }
     CU(cudaEventRecord(ev_fork, s));
     CU(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
-    if (gather) {
+    if (!gather) {
+      // the peers' rows on the TMA engines: one 1-warp CTA per SM (two 4 KB pieces in
+      // flight each; ~12 KB of shared memory, so it fits next to the GEMM's CTA)
+      launch_push_tma(a, x, b, ctx->num_sms, ctx->side);
+    } else {
       // side stream: each token row once to every rank hosting one of its experts,
       // plus the row -> token-row map entries (flag_data), then this rank's expansion
       // of the rows its peers sent, source by source as they arrive.  (Reusing the
@@ -1005,8 +1016,6 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
       launch_scatter(a, x, idx, b, 5, ctx->side, ctx->remote_ctas);
       launch_expand(a, b, ctx->remote_ctas, ctx->side);
       LAUNCHED(ctx, 1);
-    } else {
-      launch_scatter(a, x, idx, b, 2, ctx->side, ctx->remote_ctas);
     }
     tl_rec(ctx, 3, ctx->side);
     CU(cudaEventRecord(ev_join, ctx->side));

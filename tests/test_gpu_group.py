@@ -98,7 +98,7 @@ PLACEMENTS = {
 @pytest.mark.parametrize("G", [2, 4])
 def test_group_plan_payload_and_layer(cuda_ok, G, fused, dispatch, monkeypatch):
     """scatter: every routed row is stored into the hosting rank's receive row by
-    the source (NVLink); gather: every token block is copied once to every peer by
+    the source (NVLink; TMA bulk copies for the peers' rows); gather: every token block is copied once to every peer by
     the copy engines, the source sends only the row -> token map, and the receiver
     expands its rows (k_expand); fused / pulled combine."""
     monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
@@ -468,3 +468,53 @@ def test_group_direct_layer_to_layer_dispatch(cuda_ok, G):
 def synth_logits(T, E, seed):
     import synth
     return synth.zipf_logits(T, E, 1.6, seed=seed).to(DEV)
+
+
+@pytest.mark.parametrize("P,s", [([0, 1, 2, 2, 3, 2, 3, 3], 1.6), ([0, 0, 1, 1, 2, 2, 3, 3], 0.0)])
+def test_group_mixtral_full_size_every_tile(cuda_ok, P, s):
+    """The bench's 4EP configuration at full size -- Mixtral layer (E8 top-2, H4096,
+    F14336), T = 16384 tokens over 4 real P2P ranks on one GPU, ILP-1 balanced
+    placement at s = 1.6 (D3) and contiguous at s = 0 (D2) -- checked against the
+    oracle on tokens covering every 256-row M tile of every expert segment (on
+    each hosting rank, an expert's rows are ordered by source, then token: the
+    global token order, as in the virtual-rank layout)."""
+    import synth
+    from tests.test_gpu_parity import tile_cover_tokens
+    moe = _moe()
+    T, H, F, E, k, G = 16384, 4096, 14336, 8, 2, 4
+    P = np.array(P)
+    g = Group(G, T, H, F, E, k)
+    x_all = synth.hidden_states(T, H, seed=0, device=DEV)
+    logits_all = synth.zipf_logits(T, E, s, seed=0, device=DEV)
+    xs = [x_all[a:b].contiguous() for a, b in g.blocks]
+    ls = [logits_all[a:b].contiguous() for a, b in g.blocks]
+    ws_cpu = [synth.expert_weights(e, H, F, 0, device=DEV) for e in range(E)]
+    ws = []
+    for r in range(G):
+        hosted = [e for e in range(E) if P[e] == r]
+        w1 = torch.stack([ws_cpu[e][0] for e in hosted])
+        w3 = torch.stack([ws_cpu[e][1] for e in hosted])
+        ws.append((moe.pack_w13(w1, w3), torch.stack([ws_cpu[e][2] for e in hosted])))
+        g.lays[r].placement(P)
+    torch.cuda.synchronize()
+    rw = g.each(lambda r, lay: lay.route(ls[r], k))
+    g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+    g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
+    outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+    g.sync()
+    out = torch.cat(outs)
+    gidx = torch.cat([q[0] for q in rw]).cpu().numpy()
+    sel = tile_cover_tokens(gidx, E, 256, seed=7)
+    xsel = bf16_to_f64(x_all[sel])
+    cache = {}
+
+    def fn(e, rows):
+        if e not in cache:
+            cache.clear()
+            cache[e] = tuple(bf16_to_f64(m) for m in ws_cpu[e])
+        from oracle import ffn
+        return ffn.swiglu(rows, *cache[e])[1]
+    ref, ridx, _ = olayer.layer_direct(xsel, logits_all[sel].cpu().numpy(), k, fn)
+    assert np.array_equal(gidx[sel], ridx)
+    assert_close_layer(bf16_to_f64(out[sel]), ref)
+    g.close()
