@@ -38,6 +38,7 @@ constexpr int BK = 64;  // 64 bf16 = 128 bytes = one swizzle row
 constexpr int kGemmThreads = 192;
 constexpr int kSmemBudget = 200 * 1024;
 constexpr int kSchedRing = 8;  // depth of the tile-scheduler ring
+constexpr int kAhead = 8;      // k-blocks before a tile's end at which the leader publishes the next tile
 
 template <int BN, int CG, bool FUSED = false>
 struct GemmCfg {
@@ -285,9 +286,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     ++seq;
     return t;
   };
+  // A consumer's "slot read" arrival carries no data, so it is relaxed: a release at
+  // cluster scope costs the MMA issuer ~1.25k cycles per tile on its critical path
+  // (profiles/r2_k5_mma_issuer_trace*.json).  The slot's tile id was read and
+  // branched on before the arrival, so the load completed first.
   auto release_tile = [&](int seq_after) {
     const int slot = (seq_after - 1) % kSchedRing;
-    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(smem_u32(&sempty[slot]), 0));
+    if constexpr (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(&sempty[slot]), 0));
     else mbar_arrive(&sempty[slot]);
   };
   (void)cluster_id;
@@ -302,19 +307,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
       // P2P: this dispatch's flag value (written by k_layout earlier on the stream)
       const unsigned epoch = sw.flags != nullptr ? *(volatile const unsigned*)sw.epoch_ptr : 0u;
+      // The leader takes the next tile id from the global counter and publishes it to
+      // every role kAhead k-blocks before the end of the current tile: at the tile
+      // boundary the MMA issuer and the peer producer find the next tile already in
+      // the ring, and this producer goes straight on to its first loads (measured at
+      // the boundary before: the MMA issuer waited ~1.3k cycles for the id and ~0.7k
+      // for the first data, profiles/r2_k5_mma_issuer_trace.json)
+      auto fetch_publish = [&]() -> int {
+        const int slot = seq % kSchedRing;
+        mbar_wait_cluster(&sempty[slot], (uint32_t)(((seq / kSchedRing) & 1) ^ 1));
+        const int t = (int)atomicAdd(sched, 1u);
+        sched_tile[slot] = t;
+        if constexpr (CG == 2) {
+          st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)t);
+          mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[slot]), 1));
+        }
+        mbar_arrive(&sfull[slot]);
+        ++seq;
+        return t;
+      };
+      int pending = -1;  // leader: the next tile, already published
       while (true) {
         int tile;
         if (leader) {
-          const int slot = seq % kSchedRing;
-          mbar_wait_cluster(&sempty[slot], (uint32_t)(((seq / kSchedRing) & 1) ^ 1));
-          tile = (int)atomicAdd(sched, 1u);
-          sched_tile[slot] = tile;
-          if constexpr (CG == 2) {
-            st_shared_cluster_u32(mapa_shared(smem_u32(&sched_tile[slot]), 1), (uint32_t)tile);
-            mbar_arrive_cluster(mapa_shared(smem_u32(&sfull[slot]), 1));
-          }
-          mbar_arrive(&sfull[slot]);
-          ++seq;
+          tile = pending >= 0 ? pending : fetch_publish();
+          pending = -1;
         } else {
           tile = take_tile(seq);
           release_tile(seq);
@@ -350,7 +367,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (waited) asm volatile("fence.proxy.async.global;" ::: "memory");
         }
+        const int kb_next = max(kb_lo, kb_hi - kAhead);
         for (int kb = kb_lo; kb < kb_hi; ++kb) {
+          if (leader && kb == kb_next) pending = fetch_publish();
           mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (CG == 2) {
             const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -380,8 +399,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int seq = 0;
       while (true) {
         const int tile = take_tile(seq);
+        if (tile >= total_tiles) {
+          release_tile(seq);
+          break;
+        }
         release_tile(seq);
-        if (tile >= total_tiles) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
