@@ -248,3 +248,37 @@ def balance_slack(e2g, G):
     e2g = np.asarray(e2g)
     counts = np.bincount(e2g.ravel(), minlength=G)
     return float(np.abs(counts - e2g.size / G).max())
+
+
+def to_json(expert_to_gpu_, gpu_of_cluster=None, objective=None, balance_slack_=None):
+    """The portable placement file of SPEC's External Interfaces,
+    {"balance_slack", "objective", "gpu_of_cluster": [[...]], "expert_to_gpu": [[...]]}
+    -- what the paper stores as a framework-specific tensor file (§Leveraging ILP
+    optimization).  expert_to_gpu: [L][E]; gpu_of_cluster: [L][G] (identity if
+    None); the balance slack is computed when not given."""
+    import json
+    e2g = np.asarray(expert_to_gpu_, dtype=np.int64)
+    if e2g.ndim == 1:
+        e2g = e2g[None, :]
+    G = int(e2g.max()) + 1 if e2g.size else 1
+    goc = np.stack([np.arange(G)] * e2g.shape[0]) if gpu_of_cluster is None else np.asarray(gpu_of_cluster)
+    return json.dumps({"balance_slack": float(balance_slack(e2g, G) if balance_slack_ is None else balance_slack_),
+                       "objective": None if objective is None else float(objective),
+                       "gpu_of_cluster": goc.astype(int).tolist(), "expert_to_gpu": e2g.astype(int).tolist()})
+
+
+def from_json(text):
+    """Inverse of to_json: returns (expert_to_gpu int32 [L][E], the parsed dict).
+    Each row is one layer's expert_to_rank input of moe_dispatch (as a device
+    array per layer).  Rejects ragged or negative maps (S:L296-style errors)."""
+    import json
+    d = json.loads(text)
+    e2g = d.get("expert_to_gpu")
+    if not isinstance(e2g, list) or not e2g or not all(isinstance(r, list) for r in e2g):
+        raise ValueError("expert_to_gpu must be a non-empty list of per-layer lists")
+    if len({len(r) for r in e2g}) != 1:
+        raise ValueError("expert_to_gpu rows differ in length")
+    arr = np.asarray(e2g, dtype=np.int64)
+    if (arr < 0).any():
+        raise ValueError("negative GPU id in expert_to_gpu")
+    return arr.astype(np.int32), d

@@ -129,3 +129,21 @@ def test_expert_to_gpu_and_balance():
     assert e2g.tolist() == [[1, 1, 0, 0], [1, 0, 0, 1]]
     assert placement.balance_slack(e2g, 2) == 0.0
     assert placement.balance_slack(np.array([[0, 0, 0, 1]]), 2) == 1.0
+
+
+def test_placement_json_roundtrip_and_errors():
+    """SPEC's portable placement file: the per-layer expert -> GPU maps
+    round-trip; ragged or negative maps are rejected."""
+    import json
+    e2g = np.array([[0, 1, 2, 2, 3, 2, 3, 3], [1, 0, 3, 3, 2, 3, 2, 2]])
+    goc = np.array([[0, 1, 2, 3], [1, 0, 3, 2]])
+    text = placement.to_json(e2g, goc, objective=42.0)
+    d = json.loads(text)
+    assert set(d) == {"balance_slack", "objective", "gpu_of_cluster", "expert_to_gpu"}
+    back, parsed = placement.from_json(text)
+    assert back.dtype == np.int32 and back.tolist() == e2g.tolist()
+    assert parsed["gpu_of_cluster"] == goc.tolist() and parsed["objective"] == 42.0
+    assert parsed["balance_slack"] == placement.balance_slack(e2g, 4)
+    for bad in ['{"expert_to_gpu": [[0, 1], [0]]}', '{"expert_to_gpu": [[0, -1]]}', '{"expert_to_gpu": []}']:
+        with pytest.raises(ValueError):
+            placement.from_json(bad)

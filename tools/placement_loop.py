@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graph", action="store_true", help="capture each chain in a CUDA graph and time the replays")
     ap.add_argument("--direct", action="store_true", help="also time direct l -> l+1 dispatch chains (NEXT-4)")
+    ap.add_argument("--save-json", default=None, help="write the ILP 1 + ILP 2 placement (SPEC's placement JSON)")
     a = ap.parse_args()
     from paper_2502_06643_b200 import moe, placement
 
@@ -123,6 +124,9 @@ def main():
     host_s = time.perf_counter() - th
     Cc = placement.comm_costs(coact_h, contig, G)
     plans = {"contiguous": contig, "ilp1": ilp1, "ilp1+ilp2": ilp12}
+    if a.save_json and rank == 0:
+        with open(a.save_json, "w") as f:
+            f.write(placement.to_json(ilp12, goc, objective=placement.objective_o2(C1, goc)))
     o2 = {"contiguous": placement.objective_o2(Cc, goc_id), "ilp1": placement.objective_o2(C1, goc_id),
           "ilp1+ilp2": placement.objective_o2(C1, goc)}
 
