@@ -588,11 +588,13 @@ __global__ void __launch_bounds__(32) k_push_tma(PlanArgs a, const uint8_t* __re
   __syncwarp();
   uint32_t phase_bits = 0;  // bit q = phase of stage q
   const uint64_t pol = l2_evict_first_policy();
-  const int nbatch = (a.T + 31) / 32;
+  // tokens per batch: up to 32, fewer when T is small, so every CTA gets a batch
+  const int bsz = max(1, min(32, (a.T + (int)gridDim.x - 1) / (int)gridDim.x));
+  const int nbatch = (a.T + bsz - 1) / bsz;
   for (int bt = blockIdx.x; bt < nbatch; bt += gridDim.x) {
-    const int t = bt * 32 + lane;
+    const int t = bt * bsz + lane;
     int nd = 0;
-    if (t < a.T) {
+    if (lane < bsz && t < a.T) {
       for (int j = 0; j < a.k; ++j) {
         const long long gi = (long long)t * a.k + j;
         const int row = b.row_of_item[gi], slot = b.slot_of_item[gi];
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(32) k_push_tma(PlanArgs a, const uint8_t* __re
           pq[q] = pc;
           const uint32_t bar = smem_u32(&full[q]);
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(piece) : "memory");
-          bulk_g2s(smem_u32(stage_s[q]), x + (long long)(bt * 32 + l) * rowb + (long long)pc * piece, piece, bar);
+          bulk_g2s(smem_u32(stage_s[q]), x + (long long)(bt * bsz + l) * rowb + (long long)pc * piece, piece, bar);
           ++issued;
           if (++pc == npieces) {
             pc = 0;
