@@ -535,3 +535,40 @@ def test_direct_layer_to_layer_dispatch_bit_exact(cuda_ok, G):
     for li in range(L):
         xr, _, _ = olayer.layer_direct(xr, logits[li].cpu().numpy(), k, inp.oracle_expert_fn())
     assert_close_layer(bf16_to_f64(direct_out), xr)
+
+
+def test_direct_dispatch_argument_checks(cuda_ok):
+    """moe_dispatch_from's call discipline (moe.h): prev must be another context of
+    the same rank whose last FFN ran with MOE_OUT_STAY on the same T; a
+    MOE_OUT_STAY context refuses moe_combine."""
+    moe = _moe()
+    T, H, F, E, k, G = 300, 64, 128, 8, 2, 2
+    inp = Inputs(T, H, F, E, k, s=1.6, seed=81)
+    a, b = make_layer(T, H, F, E, k, G), make_layer(T, H, F, E, k, G)
+    x, logits = inp.to_device(DEV)
+    w1, w3, w2 = inp.device_weights(DEV, list(range(E)))
+    w13 = moe.pack_w13(w1, w3)
+    P = [0, 1] * 4
+    idx, w = a.route(logits, k)
+    a.dispatch(x, idx, P)
+    with pytest.raises(moe.MoeError) as ei:           # prev is not in MOE_OUT_STAY / has no FFN yet
+        b.dispatch_from(a, w, idx, P)
+    assert ei.value.status == 1
+    a.output_mode("stay")
+    a.expert_ffn(w13, w2)
+    with pytest.raises(moe.MoeError) as ei:           # the outputs stay: no home combine
+        a.combine(w)
+    assert ei.value.status == 1
+    with pytest.raises(moe.MoeError) as ei:           # prev must be another context
+        a.dispatch_from(a, w, idx, P)
+    assert ei.value.status == 1
+    with pytest.raises(moe.MoeError) as ei:           # T differs from prev's
+        b.dispatch_from(a, w[:10].contiguous(), idx[:10].contiguous(), P)
+    assert ei.value.status == 1
+    b.dispatch_from(a, w, idx, P)                     # valid
+    b.expert_ffn(w13, w2)
+    out = b.combine(w)
+    b.sync()
+    assert torch.isfinite(out.float()).all()
+    a.close()
+    b.close()
