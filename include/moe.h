@@ -123,7 +123,9 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
  * NULL = cfg->device for all; ranks on different devices use peer access.
  * Several ranks may share one device (e.g. an EP group emulated with the real
  * multi-rank data plane on one GPU): each then runs its persistent GEMM grids on
- * (SMs - 16) / (ranks on the device) SMs, so every rank's kernels co-reside.
+ * (SMs - 16) / (ranks on the device) SMs, so every rank's kernels co-reside;
+ * s ranks on one device need CUDA_DEVICE_MAX_CONNECTIONS >= 2s hardware queues
+ * (default 8: up to 4 ranks), else MOE_ERR_UNSUPPORTED.
  * cfg->world and cfg->rank are ignored; cfg->virtual_ranks must be <= 1.  Every
  * rank's calls are issued on its own stream(s); a rank's collective calls may be
  * issued from one host thread in rank order (no call blocks on a peer) -- except

@@ -680,6 +680,20 @@ moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t*
   auto devs = std::make_shared<std::vector<int>>();
   for (int r = 0; r < n; ++r)
     if (std::find(devs->begin(), devs->end(), cf[r].device) == devs->end()) devs->push_back(cf[r].device);
+  // Ranks sharing a device spin on each other's flags from different streams.  Each
+  // rank drives two streams (its caller's and its side stream); when the device has
+  // fewer hardware work queues than that, streams alias onto one queue and a spinning
+  // kernel can sit in front of the peer kernel it waits for (a flag timeout).
+  int conns = 8;   // CUDA's default
+  if (const char* cm = getenv("CUDA_DEVICE_MAX_CONNECTIONS")) conns = atoi(cm);
+  for (int d : *devs) {
+    int share = 0;
+    for (int r = 0; r < n; ++r) share += cf[r].device == d;
+    if (share > 1 && 2 * share > conns)
+      return fail(nullptr, MOE_ERR_UNSUPPORTED,
+                  "%d ranks share device %d: needs CUDA_DEVICE_MAX_CONNECTIONS >= %d (set before CUDA "
+                  "initialises; it is %d)", share, d, 2 * share, conns);
+  }
   for (int r = 0; r < n; ++r) {
     int share = 0;
     for (int q = 0; q < n; ++q) share += cf[q].device == cf[r].device;

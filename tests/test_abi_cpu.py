@@ -96,6 +96,26 @@ def test_group_create_validates_before_touching_the_device():
         assert st in (1, 5), (upd, n, st)
 
 
+def test_group_create_checks_hardware_queues(monkeypatch):
+    """s ranks of a single-process group on one device drive 2s streams that spin
+    on each other's flags: with fewer hardware queues (CUDA_DEVICE_MAX_CONNECTIONS,
+    default 8) two of them alias onto one queue and can deadlock until the flag
+    timeout, so creation refuses before touching the device."""
+    moe = _moe()
+    lib = moe.lib()
+    kw = dict(max_tokens=16, hidden=64, ffn=128, num_experts=8, max_k=2, world=1, rank=0, device=0,
+              virtual_ranks=1, a2a_mode=1, tp=1)
+    cfg = moe.Config(*[kw[f] for f, _ in moe.Config._fields_])
+    for conns, n in (("8", 5), (None, 6), ("12", 8)):
+        if conns is None:
+            monkeypatch.delenv("CUDA_DEVICE_MAX_CONNECTIONS", raising=False)
+        else:
+            monkeypatch.setenv("CUDA_DEVICE_MAX_CONNECTIONS", conns)
+        hs = (ctypes.c_void_p * n)()
+        assert lib.moe_ctx_create_group(ctypes.byref(cfg), n, None, hs) == 5
+        assert b"CUDA_DEVICE_MAX_CONNECTIONS" in lib.moe_last_error(None)
+
+
 def _layout_checks(moe, P, cnt, idx_by_source):
     G, E = cnt.shape
     seg, rb, rr, sb = moe.layout_host(P, cnt)

@@ -15,6 +15,8 @@ virtual-rank run and within 2e-2 of the oracle (G16).  Ranks are issued from
 one host thread in rank order; no call blocks on a peer.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -517,4 +519,67 @@ def test_group_mixtral_full_size_every_tile(cuda_ok, P, s):
     ref, ridx, _ = olayer.layer_direct(xsel, logits_all[sel].cpu().numpy(), k, fn)
     assert np.array_equal(gidx[sel], ridx)
     assert_close_layer(bf16_to_f64(out[sel]), ref)
+    g.close()
+
+
+RANDOM_CONFIGS = [  # (seed, G, tp, T, H, F, E, k): ragged token splits, uneven and empty ranks
+    (1, 2, 1, 257, 64, 128, 4, 1),
+    (2, 3, 1, 1031, 128, 256, 6, 2),
+    (3, 4, 1, 90, 64, 128, 16, 4),
+    (4, 4, 2, 777, 128, 256, 8, 2),
+    (5, 6, 1, 2000, 64, 192, 12, 3),
+    (6, 8, 1, 513, 64, 128, 64, 8),
+    (7, 8, 2, 300, 64, 256, 32, 4),
+    (8, 2, 2, 5, 64, 128, 8, 2),
+]
+
+
+@pytest.mark.parametrize("seed,G,tp,T,H,F,E,k", RANDOM_CONFIGS)
+def test_group_random_configs_match_virtual(cuda_ok, seed, G, tp, T, H, F, E, k):
+    """Seeded random shapes through the real P2P data plane of a single-process
+    group on one GPU: a random placement over the G/tp EP groups (some hosting
+    nothing), ragged token blocks (some ranks own none when T < G), both dispatch
+    forms; the outputs equal the virtual-rank run bit-exactly and the oracle
+    within tolerance (the TP oracle when tp > 1)."""
+    moe = _moe()
+    rng = np.random.default_rng(seed)
+    n_grp = G // tp
+    P = rng.integers(0, n_grp, E)
+    inp = Inputs(T, H, F, E, k, s=float(rng.uniform(0.0, 1.8)), seed=100 + seed)
+    g = Group(G, T, H, F, E, k, tp=tp)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    w1a, w3a, w2a = inp.device_weights(DEV, list(range(E)))
+    ws = []
+    for r in range(G):
+        hosted = [e for e in range(E) if P[e] == r // tp]
+        if not hosted:
+            ws.append((None, None))
+            continue
+        sel = torch.tensor(hosted, device=DEV)
+        if tp > 1:
+            ws.append(moe.tp_slice_weights(w1a[sel], w3a[sel], w2a[sel], tp, r % tp))
+        else:
+            ws.append((moe.pack_w13(w1a[sel], w3a[sel]), w2a[sel].contiguous()))
+    for lay in g.lays:
+        lay.placement(P)
+    torch.cuda.synchronize()
+    virt = _virtual_out(inp, P, G, k, tp=tp)
+    if tp == 1:
+        ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    else:
+        ref, _, _, _ = olayer.layer_ep_tp(bf16_to_f64(inp.x), inp.logits.numpy(), k, P, n_grp, tp,
+                                          inp.oracle_tp_fn(tp))
+    for dispatch in ("scatter", "gather"):
+        os.environ["MOE_DISPATCH"] = dispatch
+        try:
+            rw = g.each(lambda r, lay: lay.route(ls[r], k))
+            g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+            g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
+            outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+            g.sync()
+        finally:
+            os.environ.pop("MOE_DISPATCH", None)
+        out = torch.cat(outs)
+        assert torch.equal(out.view(torch.int16), virt.view(torch.int16)), dispatch
+        assert_close_layer(bf16_to_f64(out), ref)
     g.close()
