@@ -583,3 +583,72 @@ def test_group_random_configs_match_virtual(cuda_ok, seed, G, tp, T, H, F, E, k)
         assert torch.equal(out.view(torch.int16), virt.view(torch.int16)), dispatch
         assert_close_layer(bf16_to_f64(out), ref)
     g.close()
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("E,k,tp,fused", [(64, 8, 1, "1"), (8, 2, 2, "0"), (8, 2, 2, "1"), (16, 4, 1, "0")])
+def test_group_eight_ranks_over_devices(cuda_ok, E, k, tp, fused, monkeypatch):
+    """An 8-rank group over the box's GPUs (2 ranks per GPU on 4 GPUs, 4 on 2):
+    8EP at E64 top-8 (D5's shape scaled down) and 4EP-2TP (the 8-GPU TP config),
+    the P2P data plane crossing NVLink between devices and staying local between
+    the ranks of one device; bit-exact with the 8-virtual-rank run, and the
+    oracle within tolerance."""
+    nd = torch.cuda.device_count()
+    if nd < 2:
+        pytest.skip("needs >= 2 GPUs")
+    nd = 4 if nd >= 4 else 2
+    monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
+    moe = _moe()
+    G, T, H, F = 8, 3001, 256, 512
+    n_grp = G // tp
+    devs = [r * nd // G for r in range(G)]
+    inp = Inputs(T, H, F, E, k, s=1.2, seed=77 + E + tp)
+    P = np.array([(e * 5 + 3) % n_grp for e in range(E)])       # non-monotone, every group hosts experts
+    blocks = oplan.token_blocks(T, G)
+    tmax = max(b - a for a, b in blocks)
+    lays = moe.MoeLayer.group(G, max_tokens=tmax, hidden=H, ffn=F, num_experts=E, max_k=k, devices=devs, tp=tp)
+    streams = [torch.cuda.Stream(device=d) for d in devs]
+    w1a, w3a, w2a = inp.device_weights("cpu", list(range(E)))
+    xs, ls, ws = [], [], []
+    for r, (a, b) in enumerate(blocks):
+        d = torch.device("cuda", devs[r])
+        xs.append(inp.x[a:b].contiguous().to(d))
+        ls.append(inp.logits[a:b].contiguous().to(d))
+        hosted = [e for e in range(E) if P[e] == r // tp]
+        with torch.cuda.device(d):
+            w1, w3, w2 = w1a[hosted].to(d), w3a[hosted].to(d), w2a[hosted].to(d)
+            if tp > 1:
+                ws.append(moe.tp_slice_weights(w1, w3, w2, tp, r % tp))
+            else:
+                ws.append((moe.pack_w13(w1, w3), w2.contiguous()))
+            lays[r].placement(P)
+    for d in range(nd):
+        torch.cuda.synchronize(d)
+
+    def each(fn):
+        res = []
+        for r, lay in enumerate(lays):
+            with torch.cuda.device(devs[r]), torch.cuda.stream(streams[r]):
+                res.append(fn(r, lay))
+        return res
+
+    for _ in range(2):                                   # the second pass reuses the buffers (epochs)
+        rw = each(lambda r, lay: lay.route(ls[r], k))
+        each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        each(lambda r, lay: lay.expert_ffn(*ws[r]))
+        outs = each(lambda r, lay: lay.combine(rw[r][1]))
+        for lay in lays:
+            lay.sync()
+    out = torch.cat([o.cpu() for o in outs])
+    virt = _virtual_out(inp, P, G, k, tp=tp).cpu()
+    assert torch.equal(out.view(torch.int16), virt.view(torch.int16)), "8-rank group vs 8 virtual ranks"
+    if tp == 1:
+        ref, _, _ = olayer.layer_direct(bf16_to_f64(inp.x), inp.logits.numpy(), k, inp.oracle_expert_fn())
+    else:
+        ref, _, _, _ = olayer.layer_ep_tp(bf16_to_f64(inp.x), inp.logits.numpy(), k, P, n_grp, tp,
+                                          inp.oracle_tp_fn(tp))
+    assert_close_layer(bf16_to_f64(out), ref)
+    for d in range(nd):
+        torch.cuda.synchronize(d)
+    for lay in lays:
+        lay.close()
