@@ -21,7 +21,8 @@
  *   - Argument validation is synchronous: on MOE_ERR_INVALID_ARG nothing was
  *     enqueued.  moe_last_error(ctx) holds a message for the last failure.
  *   - The library never aborts and never prints.
- *   - A context is bound to one device and is not thread-safe.
+ *   - A context is bound to one device and is not thread-safe.  Calls run on
+ *     the context's device and leave the caller's current device unchanged.
  *
  * Ranks.  An EP group has G ranks.  G = config.world real processes (one per
  * GPU, NCCL between them), or G = config.virtual_ranks ranks emulated inside
@@ -130,7 +131,12 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
  * rank's calls are issued on its own stream(s); a rank's collective calls may be
  * issued from one host thread in rank order (no call blocks on a peer) -- except
  * moe_dispatch with info != NULL, moe_ctx_sync and the debug / timing reads,
- * which synchronise and so must come after every rank's calls they depend on. */
+ * which synchronise and so must come after every rank's calls they depend on.
+ * Copy-engine mode (environment MOE_A2A_CE=1, P2P, tp 1): moe_dispatch of a
+ * multi-process rank blocks until this dispatch's count matrix is known (it
+ * queues the peer copies); a group rank's moe_expert_ffn does, so every rank's
+ * moe_dispatch must precede any rank's moe_expert_ffn.  Not used while the stream
+ * is being captured into a CUDA graph. */
 moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t* devices, moe_ctx_t* out);
 /* Collective when world > 1 (starts with a barrier over the group, so no peer
  * still reads this rank's mapped buffers).  A single-process group's context
@@ -305,9 +311,12 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream);
 
 /* MOE_A2A_NCCL mode: copies the compact send buffer of the last dispatch -- this
  * rank's rows for remote experts, in the C3 send order (key P[e], e, t; G9) -- to
- * host bf16 [rows][H] (rows_host may be NULL to query *rows_out).  Other modes
- * have no send buffer (MOE_ERR_UNSUPPORTED): P2P stores rows straight into the
- * peers' receive buffers, virtual ranks into the shared receive buffer. */
+ * host bf16 [rows][H] (rows_host may be NULL to query *rows_out).  Copy-engine
+ * mode (MOE_A2A_CE, P2P): the staging buffer, indexed by the full C3 send-order
+ * slot (rows = this rank's routed items; the slots of its own experts' items are
+ * not staged); single-process groups: after the rank's moe_expert_ffn.  Other
+ * modes have no send buffer (MOE_ERR_UNSUPPORTED): P2P stores rows straight into
+ * the peers' receive buffers, virtual ranks into the shared receive buffer. */
 moe_status moe_debug_send(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out);
 
 /* Copies the received rows of the last dispatch, in unpadded receive order of

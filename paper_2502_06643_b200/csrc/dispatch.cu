@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(kMaxExperts) k_layout(PlanArgs a, PlanBuffers 
       seg_row0[pos] = (int)start;
       seg_rows[pos] = rows_s[e];
       seg_w[pos] = a.virt ? e : pos_r;
+      b.seg_e[pos] = e;
       if (start + pad_s[e] > cap_rows) atomicOr(b.err, kErrCapacity);
     }
     for (int s = 0; s < a.V; ++s) {
@@ -340,7 +341,7 @@ __device__ __forceinline__ int item_slot(const PlanArgs& a, int p) {
 
 __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __restrict__ idx, const PlanBuffers& b,
                                            int tile, int s, int t0, int t1, TileItems& it, int* run, int* wcnt,
-                                           bool write_plan) {
+                                           bool write_plan, bool ce_stage = false) {
   const int E = a.E;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
@@ -369,8 +370,11 @@ __device__ __forceinline__ void tile_ranks(const PlanArgs& a, const int32_t* __r
         slot = item_slot(a, b.P[e]);
         cslot = b.cslot_base[s * E + e] + within;
       }
-      it.row[i] = row;
-      it.slot[i] = (uint8_t)slot;
+      // copy-engine staging (mode 7): a peer's row goes to the send buffer at its
+      // send-order slot (slot marker 255), this rank's own rows to its receive rows
+      const bool to_send = ce_stage && row >= 0 && slot != a.me;
+      it.row[i] = to_send ? cslot : row;
+      it.slot[i] = to_send ? (uint8_t)255 : (uint8_t)slot;
       if (write_plan) {
         b.row_of_item[(long long)t0 * a.k + i] = row;
         b.slot_of_item[(long long)t0 * a.k + i] = (uint8_t)slot;
@@ -413,7 +417,8 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   // covers this rank's items on the caller's stream: modes 0 and 1, or -- direct
   // dispatch, which copies no rows -- mode 6
   tile_ranks(a, idx, b, tile, s, t0, t1, it, run, wcnt,
-             part == 0 && (mode == 0 || (mode == 1 && !a.plan_done) || mode == 3 || mode == 6));
+             part == 0 && (mode == 0 || (mode == 1 && !a.plan_done) || mode == 3 || mode == 6 || mode == 7),
+             mode == 7);
   if (mode == 3) {  // plan arrays only
     __syncthreads();
     continue;
@@ -490,7 +495,7 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
   // all-gather inside the dispatch); otherwise a slot is one destination buffer
   const bool fan = a.p2p && a.tp > 1;
   const bool local_only = mode == 1;
-  if (mode != 0) {  // drop the rows the other kernel copies
+  if (mode != 0 && mode != 7) {  // drop the rows the other kernel copies
     const int n = (t1 - t0) * a.k;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       if (it.row[i] < 0) continue;
@@ -527,7 +532,8 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_scatter(PlanArgs a, cons
           const int row = it.row[i];
           if (row < 0) continue;
           if (!fan) {
-            dst_s[it.slot[i]][(long long)row * cpr + c] = v[u];
+            uint4* d = it.slot[i] == 255 ? b.sendbuf : dst_s[it.slot[i]];
+            d[(long long)row * cpr + c] = v[u];
           } else {
             const int r0 = it.slot[i] * a.tp;
             for (int q = 0; q < a.tp; ++q) {
@@ -868,17 +874,21 @@ __global__ void __launch_bounds__(kScatterThreads, 2) k_combine(PlanArgs a, cons
   // source of partial q of an item with slot sl: src_s[sl * tp + q].  P2P pull: the
   // expert-output buffer of rank sl*tp+q; fused: the return buffer of slice q
   // (slot 0); virtual: the expert-output buffer of slice q (slot 0); NCCL: slot.
-  const int nslots = (a.p2p && !a.fused) ? a.G : (a.tp > 1 ? a.tp : 2);
+  const int nslots = a.ce ? 2 : (a.p2p && !a.fused) ? a.G : (a.tp > 1 ? a.tp : 2);
   for (int q = threadIdx.x; q < nslots; q += blockDim.x)
-    src_s[q] = a.fused ? b.ret_local + q * b.part_stride
-                       : ((a.virt && a.tp > 1) ? b.src_table[0] + q * b.part_stride : b.src_table[q]);
+    src_s[q] = a.ce ? (q == 0 ? b.ret_local : b.src_table[a.me])
+               : a.fused ? b.ret_local + q * b.part_stride
+                         : ((a.virt && a.tp > 1) ? b.src_table[0] + q * b.part_stride : b.src_table[q]);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const long long gi = (long long)t0 * k + i;
-    // fused combine: K6 already stored the row into this rank's return buffer at the C3 slot
-    const int v = a.fused ? b.cslot_of_item[gi] : b.row_of_item[gi];
+    // fused combine: K6 already stored the row into this rank's return buffer at the C3
+    // slot; copy-engine combine: the peers' rows were copied there, this rank's own rows
+    // stay in its expert-output buffer
+    const bool own = a.ce && b.slot_of_item[gi] == a.me;
+    const int v = own ? b.row_of_item[gi] : (a.fused || a.ce) ? b.cslot_of_item[gi] : b.row_of_item[gi];
     row_s[i] = v;
     w_s[i] = v < 0 ? 0.f : w[gi];
-    slot_s[i] = a.fused ? 0 : b.slot_of_item[gi];
+    slot_s[i] = a.ce ? (own ? 1 : 0) : a.fused ? 0 : b.slot_of_item[gi];
   }
   if (a.p2p) wait_flags_geq(b.my_sig->flag_y, a.G, cur_epoch(a.epoch_ptr), b.err, a.timeout_ns, kWaitOutputs);
   __syncthreads();

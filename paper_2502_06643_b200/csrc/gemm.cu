@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int seq = 0;
       unsigned long long ready = 0;  // P2P: source ranks whose rows have arrived
+      int ready_seg = -1;            // (per-(source, segment) flags: `ready` holds for this segment)
       // P2P: this dispatch's flag value (written by k_layout earlier on the stream)
       const unsigned epoch = sw.flags != nullptr ? *(volatile const unsigned*)sw.epoch_ptr : 0u;
       // The leader takes the next tile id from the global counter and publishes it to
@@ -348,15 +349,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // tile holds (system-scope acquire of their arrival flags), then order
           // those generic-proxy arrivals before the TMA (async proxy) reads
           const int32_t* ss = sw.seg_src + (long long)seg * sw.G * 3;
+          if (sw.flags_se != nullptr && seg != ready_seg) {  // per-(source, segment) flags
+            ready = 0;
+            ready_seg = seg;
+          }
           bool waited = false;
           for (int s = 0; s < sw.G; ++s) {
             if (s == sw.me || ((ready >> s) & 1ull)) continue;
             const int r0 = __ldg(ss + 3 * s), n = __ldg(ss + 3 * s + 1);
             if (n == 0 || r0 >= a_row + 128 || r0 + n <= a_row) continue;
+            const unsigned* word = sw.flags_se != nullptr ? sw.flags_se + s * sw.E + __ldg(sw.seg_e + seg) : sw.flags + s;
             const unsigned long long t0 = globaltimer_ns();
             unsigned v;
             do {
-              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sw.flags + s) : "memory");
+              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(word) : "memory");
               if (globaltimer_ns() - t0 > sw.timeout_ns) {
                 atomicOr(err, timeout_bits(kWaitRowsK5));
                 break;
@@ -441,6 +447,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int ce_pending = -1;  // copy-engine combine: segment of this warp's last tile, not yet counted
     const uint32_t tempty_leader0 = (CG == 2) ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
     int seq = 0;
     while (true) {
@@ -564,6 +571,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader0 + acc * 8);
           else mbar_arrive(&tempty[acc]);
         }
+        if (fr.segdone != nullptr && ksplit == 1 && lane == 0) {
+          // copy-engine combine (after the accumulator is released): the previous
+          // tile's stores of this warp -- every bulk group but this tile's BN / 32 --
+          // are complete, then its segment's counter moves (one tile late, so the warp
+          // never waits for the stores it has just issued; the copy engines read
+          // through L2, a GPU-scope release orders them)
+          if (ce_pending >= 0) {
+            asm volatile("cp.async.bulk.wait_group %0;" ::"n"(BN / 32) : "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(fr.segdone + ce_pending) : "memory");
+          }
+          ce_pending = seg;
+        }
       }
       if (++acc == 2) {
         acc = 0;
@@ -576,6 +596,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __threadfence_system();
     } else {                // the epilogue's TMA stores have landed before the kernel ends
       if (lane == 0) bulk_wait_all();
+      if (lane == 0 && ce_pending >= 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(fr.segdone + ce_pending) : "memory");
+      }
       __syncwarp();
     }
   }

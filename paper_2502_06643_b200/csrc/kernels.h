@@ -20,6 +20,8 @@ struct SigBlock {
   unsigned phash[64];         // phash[s] = hash of the placement source s dispatched with
   unsigned flag_exp[64];      // gather dispatch: flag_exp[s] = epoch once this rank expanded source
                               // s's token rows into its receive layout (local flag; [me] too)
+  unsigned flag_se[64 * 256]; // copy-engine dispatch: flag_se[s][e] = epoch once source s's rows
+                              // for expert e landed here (a stream memory write after the copy)
 };
 
 // Dispatch plan arguments shared by K2/K3/K8 (dispatch.cu).
@@ -47,6 +49,9 @@ struct PlanArgs {
   unsigned long long timeout_ns;  // bound on every P2P flag wait (latches MOE_ERR_TIMEOUT)
   int direct;     // direct layer l -> l+1 dispatch (moe_dispatch_from): the receive rows are
                   // combined on the hosting rank from layer l's expert outputs (k_expand_direct)
+  int ce;         // copy-engine data plane (P2P): K3 stages the peers' rows in the send buffer
+                  // (send order) for the copy engines; K8 reads the peers' returned rows from the
+                  // return buffer and this rank's own rows from its expert-output buffer
 };
 
 // Device-side plan state (allocated by the context).
@@ -69,6 +74,7 @@ struct PlanBuffers {
   int* err;
   // fused combine (P2P): K6 stores each expert-output row straight into the
   // source rank's return buffer at the item's send-order slot (C3 slot)
+  uint4* sendbuf;                 // copy-engine mode: the staged peers' rows, in send order
   int32_t* seg_src;               // [E][G][3]: per hosted segment and source: first row, rows, first slot
   int32_t* cslot_base;            // [V][E] send-order slot of local source s's first item for expert e
   int32_t* cslot_of_item;         // [T*k] send-order slot (C3) of every item (within its source)
@@ -99,12 +105,18 @@ struct PlanBuffers {
   const uint4* const* prev_src;   // layer l's expert-output buffers by slot (this rank's table)
   const unsigned* prev_flag_y;    // layer l's flag_y in this rank's layer-l signal block (P2P)
   const unsigned* prev_epoch;     // layer l's flag epoch
+  int32_t* seg_e;                 // [E] global expert id of hosted segment i (k_layout)
 };
 
 // K5 per-tile arrival waits (P2P overlap): the producer waits only for the source
 // ranks whose rows a tile reads; tiles holding only this rank's own rows run first.
 struct SrcWait {
   const unsigned* flags;          // SigBlock::flag_data [G] of this rank; nullptr = no waits
+  // copy-engine dispatch: wait per (source, segment) on flags_se[s * E + seg_e[seg]]
+  // instead (nullptr: per source on flags)
+  const unsigned* flags_se;
+  const int32_t* seg_e;
+  int E;
   const int32_t* seg_src;         // see PlanBuffers::seg_src
   int G;
   int me;
@@ -118,6 +130,10 @@ struct FusedRet {
   const int32_t* seg_src;         // see PlanBuffers::seg_src
   int G;
   int enabled;
+  // copy-engine combine (plain stores): every epilogue warp adds 1 to segdone[segment]
+  // once its stores of a tile have completed, so the copy engines' stream (waiting on
+  // the value with cuStreamWaitValue32) returns a segment's rows as soon as it is done
+  unsigned* segdone;
 };
 
 // Load every kernel of the library onto the current device now (CUDA 12 loads

@@ -136,6 +136,22 @@ struct moe_ctx {
   int32_t* desc = nullptr;
   int32_t** desc_table = nullptr;       // device [max(G, 1)]
   bool last_direct = false;             // the last dispatch was moe_dispatch_from
+  // copy-engine data plane (MOE_A2A_CE, P2P): the dispatch stages the peers' rows in
+  // the send buffer; moe_expert_ffn reads the count matrix on the host and queues, on
+  // the side stream, one peer copy per (destination, expert) run plus a flag write per
+  // destination, and for the combine, per hosted segment, a wait on K6's segment
+  // counter and one copy per source run, then flag_y on every rank.  The copy engines
+  // move the rows, so no SM shares its TMA unit or issue slots with the GEMMs.
+  bool last_ce = false;
+  cudaEvent_t ev_cnt = nullptr, ev_staged = nullptr, ev_k6 = nullptr, ev_side2 = nullptr;
+  cudaStream_t side2 = nullptr;         // second copy-engine stream (the combine's runs alternate)
+  int32_t* ce_pinned = nullptr;         // host: count matrix [G][E], placement [E], epoch
+  unsigned* segdone = nullptr;          // [E] K6 per-segment completion counters
+  std::vector<void*> recv_h, sig_h, ret_h;  // host copies of the peer tables (P2P)
+  bool ce_dispatched = false;           // this dispatch's copies are queued
+  int32_t* seg_e = nullptr;             // [E] global expert of hosted segment i (device)
+  unsigned ce_epoch = 0;
+  std::vector<int32_t> ce_recv_base, ce_send_base;  // layout of the last dispatch (host)
   bool out_stay = false;                // MOE_OUT_STAY: outputs stay for moe_dispatch_from
   bool ffn_done = false;                // moe_expert_ffn ran after the last dispatch
   unsigned long long flag_timeout_ns = kFlagTimeoutNs;  // MOE_FLAG_TIMEOUT_MS overrides
@@ -146,6 +162,7 @@ struct moe_ctx {
   // with more than one CTA spins on a peer flag.
   bool local_group = false;
   bool shared_dev = false;
+  int share = 1;                        // ranks of this process's group on this device
   std::shared_ptr<std::vector<int>> group_devices;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // the same pair for layers captured into a CUDA graph (an event recorded inside a
@@ -218,6 +235,8 @@ static PlanBuffers plan_buffers(moe_ctx_t c) {
   b.seg_src = c->seg_src;
   b.cslot_base = c->cslot_base;
   b.cslot_of_item = c->cslot_of_item;
+  b.sendbuf = reinterpret_cast<uint4*>(c->sendbuf);
+  b.seg_e = c->seg_e;
   b.ret_local = reinterpret_cast<const uint4*>(c->retbuf);
   b.part_stride = c->virt ? c->cap_rows * c->H / 8 : c->send_rows * c->H / 8;
   b.recv_local = reinterpret_cast<uint4*>(c->recv);
@@ -253,6 +272,7 @@ static PlanArgs plan_args(moe_ctx_t c, int T, int k) {
   a.fused = c->p2p && c->ffn_fused;
   a.gather = 0;
   a.direct = 0;
+  a.ce = c->p2p && c->last_ce && !c->ffn_fused;  // K8: the copy engines returned the peers' rows
   a.plan_done = 0;
   a.timeout_ns = c->flag_timeout_ns;
   // enough CTAs for the HBM/NVLink-bound row copies, but no partial second wave:
@@ -358,6 +378,18 @@ static moe_status layout_host_impl(int32_t E, int32_t G, const int32_t* P, const
   return MOE_OK;
 }
 
+// Every API call that selects the context's device restores the caller's current
+// device on return (a single-process group drives several devices from one thread).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 // Configuration checks shared by moe_ctx_create and moe_ctx_create_group.
 static moe_status check_cfg(const moe_config& c) {
   moe_ctx_t ctx = nullptr;
@@ -424,6 +456,7 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
     // grids, 16 SMs stay free for the peers' row copies, so a GEMM CTA waiting for a
     // peer's rows never blocks the kernel that delivers them
     ctx->shared_dev = true;
+    ctx->share = share;
     ctx->num_sms = std::max(2, ((ctx->num_sms - 16) / share) & ~1);
     ctx->remote_ctas = std::max(1, std::min(ctx->remote_ctas, ctx->num_sms / 2));
   }
@@ -476,6 +509,7 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
             A((void**)&ctx->seg_src, sizeof(int32_t) * 3 * (size_t)E * G) &&
             A((void**)&ctx->cslot_base, sizeof(int32_t) * (size_t)ctx->V * E) &&
             A((void**)&ctx->cslot_of_item, sizeof(int32_t) * (size_t)std::max<int64_t>(Tm * k, 1)) &&
+            A((void**)&ctx->seg_e, sizeof(int32_t) * (size_t)E) &&
             A((void**)&ctx->ret_table, sizeof(void*) * (size_t)G) &&
             A((void**)&ctx->epoch_dev, sizeof(unsigned)) &&
             A((void**)&ctx->desc, sizeof(int32_t) * 3 * (size_t)k * ctx->cap_rows) &&
@@ -487,7 +521,9 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
   cudaMemset(ctx->epoch_dev, 0, sizeof(unsigned));
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_all_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess)
+      cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->ce_pinned, sizeof(int32_t) * ((size_t)G * E + E + 1)) != cudaSuccess ||
+      cudaMalloc((void**)&ctx->segdone, sizeof(unsigned) * (size_t)E) != cudaSuccess)
     return fail(ctx, MOE_ERR_CUDA, "cudaMallocHost failed");
   ctx->P_host.assign(E, 0);
   ctx->cnt_host.assign((size_t)G * E, 0);
@@ -529,6 +565,11 @@ static moe_status p2p_streams(moe_ctx_t ctx) {
   CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_fork_cap, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_join_cap, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_cnt, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_staged, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_k6, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_side2, cudaEventDisableTiming));
+  CU(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
   return MOE_OK;
 }
 
@@ -543,10 +584,14 @@ static moe_status upload_tables(moe_ctx_t ctx, std::vector<void*>& dst, std::vec
   CU(cudaMemcpy(ctx->peer_sig, sig.data(), sizeof(void*) * ctx->G, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->ret_table, ret.data(), sizeof(void*) * ctx->G, cudaMemcpyHostToDevice));
   CU(cudaDeviceSynchronize());
+  ctx->recv_h.assign(dst.begin(), dst.begin() + std::min<size_t>(dst.size(), ctx->G));
+  ctx->sig_h.assign(sig.begin(), sig.begin() + ctx->G);
+  ctx->ret_h.assign(ret.begin(), ret.begin() + ctx->G);
   return MOE_OK;
 }
 
 moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* out) {
+  DeviceGuard device_guard;
   moe_ctx_t ctx = nullptr;
   if (!cfg || !out) return fail(ctx, MOE_ERR_INVALID_ARG, "cfg/out is NULL");
   const moe_config& c = *cfg;
@@ -654,6 +699,7 @@ moe_status moe_ctx_create(const moe_config* cfg, const uint8_t* uid, moe_ctx_t* 
 }
 
 moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t* devices, moe_ctx_t* out) {
+  DeviceGuard device_guard;
   moe_ctx_t ctx = nullptr;
   if (!cfg || !out) return fail(ctx, MOE_ERR_INVALID_ARG, "cfg/out is NULL");
   if (n < 2 || n > kMaxWorld) return fail(ctx, MOE_ERR_INVALID_ARG, "n=%d outside [2, %d]", n, kMaxWorld);
@@ -749,6 +795,7 @@ moe_status moe_ctx_create_group(const moe_config* cfg, int32_t n, const int32_t*
 }
 
 moe_status moe_ctx_destroy(moe_ctx_t ctx) {
+  DeviceGuard device_guard;
   if (!ctx) return MOE_OK;
   if (ctx->comm && ctx->cfg.world > 1) {
     // collective: no peer may still read this rank's mapped buffers (a slower peer's
@@ -784,7 +831,7 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
                  ctx->sendbuf, ctx->retbuf, ctx->slot_of_item, ctx->dst_table, ctx->src_table, ctx->peer_sig,
                  ctx->sig, ctx->done_counter, ctx->seg_src, ctx->cslot_base, ctx->cslot_of_item, ctx->ret_table,
                  ctx->epoch_dev, ctx->splitk_ws, ctx->tokbuf, ctx->xmap, ctx->xmap_table, ctx->exp_counter,
-                 ctx->desc, ctx->desc_table, ctx->tok_table};
+                 ctx->desc, ctx->desc_table, ctx->tok_table, ctx->seg_e};
   for (void* p : dev)
     if (p) cudaFree(p);
   for (auto& e : ctx->ev)
@@ -793,6 +840,13 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->P_all_pinned) cudaFreeHost(ctx->P_all_pinned);
   if (ctx->cnt_pinned) cudaFreeHost(ctx->cnt_pinned);
+  if (ctx->ce_pinned) cudaFreeHost(ctx->ce_pinned);
+  if (ctx->segdone) cudaFree(ctx->segdone);
+  if (ctx->ev_cnt) cudaEventDestroy(ctx->ev_cnt);
+  if (ctx->ev_staged) cudaEventDestroy(ctx->ev_staged);
+  if (ctx->ev_k6) cudaEventDestroy(ctx->ev_k6);
+  if (ctx->ev_side2) cudaEventDestroy(ctx->ev_side2);
+  if (ctx->side2) cudaStreamDestroy(ctx->side2);
   delete ctx;
   return MOE_OK;
 }
@@ -822,6 +876,7 @@ static moe_status check_device_error(moe_ctx_t ctx) {
 }
 
 moe_status moe_ctx_sync(moe_ctx_t ctx) {
+  DeviceGuard device_guard;
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
   CU(cudaSetDevice(ctx->cfg.device));
   CU(cudaStreamSynchronize(ctx->last_stream));
@@ -832,6 +887,8 @@ moe_status moe_route(moe_ctx_t ctx, const float* logits, int32_t T, int32_t E, i
                      moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
   if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   if (E != ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "E=%d != context E=%d", E, ctx->E);
   if (k < 1 || k > E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
   if (T > 0 && (!logits || !idx || !w)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
@@ -846,6 +903,8 @@ moe_status moe_route(moe_ctx_t ctx, const float* logits, int32_t T, int32_t E, i
 moe_status moe_route_stats(moe_ctx_t ctx, const int32_t* idx_l, const int32_t* idx_l1, int32_t T, int32_t E,
                            int32_t k, int64_t* load, int64_t* coact, moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   if (T < 0 || T > ctx->cfg.max_tokens) return fail(ctx, MOE_ERR_CAPACITY, "T=%d outside [0, max_tokens]", T);
   if (E != ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "E=%d != context E=%d", E, ctx->E);
   if (k < 1 || k > E || k > ctx->cfg.max_k) return fail(ctx, MOE_ERR_INVALID_ARG, "k=%d outside [1, min(E, max_k)]", k);
@@ -861,6 +920,8 @@ moe_status moe_route_stats(moe_ctx_t ctx, const int32_t* idx_l, const int32_t* i
 
 moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E, moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   if (E != ctx->E || !load) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
@@ -876,6 +937,8 @@ moe_status moe_stats_allreduce(moe_ctx_t ctx, int64_t* load, int64_t* coact, int
 moe_status moe_stats_allreduce_layers(moe_ctx_t ctx, int64_t* load, int64_t* coact, int32_t E, int32_t L,
                                       moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   if (E != ctx->E || !load || L < 1) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
@@ -902,9 +965,12 @@ moe_status moe_pack_w13(const moe_bf16* w1, const moe_bf16* w3, int32_t n, int32
 
 // moe_dispatch (prev == NULL) and moe_dispatch_from (prev = layer l's context: the
 // rows are combined from layer l's expert outputs on the hosting ranks, NEXT-4).
+static moe_status ce_dispatch_copies(moe_ctx_t ctx);
+
 static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t* idx, int32_t T, int32_t k,
                                 const int32_t* expert_to_rank, moe_dispatch_info* info, cudaStream_t s,
                                 moe_ctx_t prev, const float* w_prev) {
+  DeviceGuard device_guard;
   const int E = ctx->E, G = ctx->G, H = ctx->H;
   const bool direct = prev != nullptr;
   const int n_grp = G / ctx->tp;  // EP ranks (groups of tp ranks when tp > 1)
@@ -937,6 +1003,21 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
   if (direct) gather = false;
   ctx->last_gather = gather;
   ctx->last_direct = direct;
+  // copy-engine data plane (opt-in, MOE_A2A_CE=1): plain EP (tp 1) with 256-row GEMM
+  // tiles, outside CUDA-graph capture (moe_expert_ffn reads the counts on the host)
+  bool ce = false;
+  if (ctx->p2p && !gather && !direct && ctx->tp == 1 && ctx->gemm_cg == 2) {
+    if (const char* env = getenv("MOE_A2A_CE")) ce = atoi(env) != 0;
+    // ranks sharing a device: three streams each (caller, side, side2) must not alias
+    // onto one hardware queue -- a copy stream's value wait would block the GEMM behind it
+    int conns = 8;
+    if (const char* cm = getenv("CUDA_DEVICE_MAX_CONNECTIONS")) conns = atoi(cm);
+    if (ctx->share > 1 && 3 * ctx->share > conns) ce = false;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CU(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) ce = false;
+  }
+  ctx->last_ce = ce;
   PlanArgs a = plan_args(ctx, T, k);
   a.gather = gather ? 1 : 0;
   a.direct = direct ? 1 : 0;
@@ -981,6 +1062,13 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
   }
   launch_layout(a, b, ctx->cap_rows, s);  // validates P; P2P: also the in-kernel count all-gather
   tl_rec(ctx, 1, s);
+  if (ce) {  // the count matrix, placement and flag epoch of this dispatch, for the host
+    CU(cudaMemcpyAsync(ctx->ce_pinned, ctx->sig->cnt, sizeof(int32_t) * G * E, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ctx->ce_pinned + (size_t)G * E, ctx->P_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ctx->ce_pinned + (size_t)G * E + E, ctx->epoch_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                       s));
+    CU(cudaEventRecord(ctx->ev_cnt, s));
+  }
   if (direct && !ctx->p2p) {
     // virtual ranks / one rank: descriptors, then every receive row combined in place
     launch_scatter(a, x, idx, b, 6, s);
@@ -1006,6 +1094,19 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
     CU(cudaStreamWaitEvent(s, ev_join, 0));
     tl_rec(ctx, 2, s);
     LAUNCHED(ctx, 2);
+  } else if (ce) {
+    // copy-engine mode: this rank's own rows into its receive rows, the peers' rows
+    // into the send buffer in send order; moe_expert_ffn queues the copies
+    launch_scatter(a, x, idx, b, 7, s);
+    CU(cudaEventRecord(ctx->ev_staged, s));
+    tl_rec(ctx, 2, s);
+    tl_rec(ctx, 3, s);
+    LAUNCHED(ctx, 1);
+    ctx->ce_dispatched = false;
+    if (!ctx->local_group) {
+      moe_status st = ce_dispatch_copies(ctx);
+      if (st != MOE_OK) return st;
+    }
   } else if (ctx->p2p) {
     // rows for peers: NVLink stores on the side stream (arrival flags raised by its
     // last CTA); rows hosted here: on `stream`, so K5 can start on them right away
@@ -1145,8 +1246,149 @@ moe_status moe_set_output_mode(moe_ctx_t ctx, int32_t mode) {
   return MOE_OK;
 }
 
+// Stream memory operations (driver API, through the runtime's entry-point query):
+// a copy-engine stream raises a peer's arrival flag after its copies
+// (cuStreamWriteValue32, with its default memory barrier) and waits for K6's segment
+// counters (cuStreamWaitValue32, GEQ).
+typedef int (*PfnStreamValue32)(cudaStream_t, unsigned long long, unsigned, unsigned);
+static PfnStreamValue32 stream_op(const char* name);
+// the address of a SigBlock field in rank r's signal block (peer mapping)
+static unsigned long long ce_flag(moe_ctx_t ctx, int r, const unsigned* field) {
+  const size_t off = reinterpret_cast<const char*>(field) - reinterpret_cast<const char*>(ctx->sig);
+  return (unsigned long long)(reinterpret_cast<char*>(ctx->sig_h[r]) + off);
+}
+static PfnStreamValue32 stream_op(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<PfnStreamValue32>(p);
+}
+
+// Copy-engine data plane, host half (MOE_A2A_CE; see moe_ctx::last_ce).
+// ce_dispatch_copies: blocks until this dispatch's count matrix is on the host, then
+// queues on the side stream, per destination rank (rotated from me + 1), one peer copy
+// per hosted expert run of the staged send buffer into the destination's receive rows,
+// then flag_data[me] = epoch on the destination (K5 there waits per tile for it).
+// Called at the end of moe_dispatch (the scatter staging the rows is already queued,
+// so the GPU works while the host waits), or -- single-process groups, whose ranks'
+// calls come from one thread in rank order -- by the rank's moe_expert_ffn.
+static moe_status ce_dispatch_copies(moe_ctx_t ctx) {
+  static PfnStreamValue32 write32 = stream_op("cuStreamWriteValue32");
+  if (!write32) return fail(ctx, MOE_ERR_UNSUPPORTED, "stream memory operations unavailable");
+  const int E = ctx->E, G = ctx->G, H = ctx->H, me = ctx->me;
+  CU(cudaEventSynchronize(ctx->ev_cnt));
+  const int32_t* cnt = ctx->ce_pinned;
+  const int32_t* P = cnt + (size_t)G * E;
+  ctx->ce_epoch = (unsigned)cnt[(size_t)G * E + E];
+  for (int e = 0; e < E; ++e)
+    if (P[e] < 0 || P[e] >= G) return fail(ctx, MOE_ERR_DEVICE, "expert_to_rank[%d]=%d outside [0, %d)", e, P[e], G);
+  ctx->cnt_host.assign(cnt, cnt + (size_t)G * E);
+  ctx->P_host.assign(P, P + E);
+  ctx->ce_recv_base.resize((size_t)G * E);
+  ctx->ce_send_base.resize((size_t)G * E);
+  layout_host_impl(E, G, P, cnt, ctx->seg_align, nullptr, ctx->ce_recv_base.data(), nullptr,
+                   ctx->ce_send_base.data());
+  cudaStream_t cs = ctx->side;
+  const size_t rowb = (size_t)H * 2;
+  CU(cudaStreamWaitEvent(cs, ctx->ev_staged, 0));
+  // the destinations' expert runs interleaved (round j: the j-th hosted expert of every
+  // destination, rotated from me + 1), each followed by its (me, e) flag: every
+  // receiver gets its segments in K5's order, at the same pace
+  std::vector<std::vector<int>> runs(G);
+  for (int e = 0; e < E; ++e)
+    if (P[e] != me && cnt[me * E + e] > 0) runs[P[e]].push_back(e);
+  size_t rounds = 0;
+  for (auto& r : runs) rounds = std::max(rounds, r.size());
+  for (size_t j = 0; j < rounds; ++j)
+    for (int q = 1; q < G; ++q) {
+      const int g = (me + q) % G;
+      if (j >= runs[g].size()) continue;
+      const int e = runs[g][j];
+      const int n = cnt[me * E + e];
+      CU(cudaMemcpyAsync(static_cast<char*>(ctx->recv_h[g]) + (size_t)ctx->ce_recv_base[me * E + e] * rowb,
+                         reinterpret_cast<char*>(ctx->sendbuf) + (size_t)ctx->ce_send_base[me * E + e] * rowb,
+                         n * rowb, cudaMemcpyDeviceToDevice, cs));
+      if (write32(cs, ce_flag(ctx, g, ctx->sig->flag_se + me * E + e), ctx->ce_epoch, 0) != 0)
+        return fail(ctx, MOE_ERR_CUDA, "cuStreamWriteValue32 failed");
+    }
+  for (int g = 0; g < G; ++g)  // every row of this dispatch sent (identity FFN, debug reads)
+    if (write32(cs, ce_flag(ctx, g, ctx->sig->flag_data + me), ctx->ce_epoch, 0) != 0)
+      return fail(ctx, MOE_ERR_CUDA, "cuStreamWriteValue32 failed");
+  CU(cudaEventRecord(ctx->cur_join, cs));
+  ctx->ce_dispatched = true;
+  return MOE_OK;
+}
+
+// ce_combine_copies: called by moe_expert_ffn after K6 is queued (outputs: 0 = this
+// rank hosts nothing; 1 = K6 was launched after ev_k6 and counts its tiles per
+// segment; 2 = the outputs are complete once the caller's stream reaches this point --
+// the identity FFN).  Queues on the side stream, per hosted segment (K6's tile order),
+// a wait on the segment's counter (every epilogue warp of every tile) and one copy per
+// source run of the expert-output rows into the source's return buffer at its
+// send-order slot; then flag_y[me] = epoch on every rank (K8 there reads the return
+// buffer, and this rank's own rows from its expert-output buffer).
+static moe_status ce_combine_copies(moe_ctx_t ctx, int outputs) {
+  static PfnStreamValue32 write32 = stream_op("cuStreamWriteValue32");
+  static PfnStreamValue32 wait32 = stream_op("cuStreamWaitValue32");
+  if (!write32 || !wait32) return fail(ctx, MOE_ERR_UNSUPPORTED, "stream memory operations unavailable");
+  if (!ctx->ce_dispatched) {
+    moe_status st = ce_dispatch_copies(ctx);
+    if (st != MOE_OK) return st;
+  }
+  ctx->ce_dispatched = false;
+  const int E = ctx->E, G = ctx->G, H = ctx->H, me = ctx->me;
+  const int32_t* cnt = ctx->cnt_host.data();
+  const int32_t* P = ctx->P_host.data();
+  cudaStream_t cs = ctx->side;
+  const size_t rowb = (size_t)H * 2;
+  if (outputs == 2) CU(cudaEventRecord(ctx->ev_k6, ctx->last_stream));
+  if (outputs > 0) {
+    // two copy streams, the segments alternating between them, so one segment's copies
+    // run while the other stream waits for the next segment
+    CU(cudaStreamWaitEvent(cs, ctx->ev_k6, 0));
+    CU(cudaStreamWaitEvent(ctx->side2, ctx->ev_k6, 0));
+    const int bn = gemm_block_n(H, false), tile_m = 128 * ctx->gemm_cg;
+    int i = 0, used2 = 0;
+    for (int e = 0; e < E; ++e) {
+      if (P[e] != me) continue;
+      int64_t rows = 0;
+      for (int src = 0; src < G; ++src) rows += cnt[src * E + e];
+      const unsigned target = (unsigned)(((rows + tile_m - 1) / tile_m) * (H / bn) * 4 * ctx->gemm_cg);
+      if (target > 0 && !ctx->out_stay) {
+        cudaStream_t st = (i & 1) ? ctx->side2 : cs;
+        used2 |= i & 1;
+        if (outputs == 1 && wait32(st, (unsigned long long)(ctx->segdone + i), target, 0) != 0)
+          return fail(ctx, MOE_ERR_CUDA, "cuStreamWaitValue32 failed");
+        for (int src = 0; src < G; ++src) {
+          const int n = cnt[src * E + e];
+          if (src == me || n == 0) continue;
+          CU(cudaMemcpyAsync(static_cast<char*>(ctx->ret_h[src]) + (size_t)ctx->ce_send_base[src * E + e] * rowb,
+                             reinterpret_cast<char*>(ctx->ybuf) + (size_t)ctx->ce_recv_base[src * E + e] * rowb,
+                             n * rowb, cudaMemcpyDeviceToDevice, st));
+        }
+      }
+      ++i;
+    }
+    CU(cudaEventRecord(ctx->ev_side2, ctx->side2));
+    CU(cudaStreamWaitEvent(cs, ctx->ev_side2, 0));
+    (void)used2;
+    if (ctx->out_stay && i > 0 && outputs == 1) {  // outputs stay here: flag_y once the whole K6 is done
+      CU(cudaEventRecord(ctx->ev_k6, ctx->last_stream));
+      CU(cudaStreamWaitEvent(cs, ctx->ev_k6, 0));
+    }
+  }
+  for (int r = 0; r < G; ++r)
+    if (write32(cs, ce_flag(ctx, r, ctx->sig->flag_y + me), ctx->ce_epoch, 0) != 0)
+      return fail(ctx, MOE_ERR_CUDA, "cuStreamWriteValue32 failed");
+  CU(cudaEventRecord(ctx->cur_join, cs));
+  return MOE_OK;
+}
+
 moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2, int32_t n_w, moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_expert_ffn before moe_dispatch");
   if (n_w < 0 || n_w > ctx->E) return fail(ctx, MOE_ERR_INVALID_ARG, "n_w=%d outside [0, E]", n_w);
   if (ctx->virt && n_w != ctx->E)
@@ -1175,7 +1417,10 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
     // device), and in P2P mode every rank still hears "my outputs are ready"
     launch_expect_nseg(ctx->seg_meta, 0, ctx->err_dev, s);
     LAUNCHED(ctx, 1);
-    if (ctx->p2p) {
+    if (ctx->last_ce) {
+      moe_status st = ce_combine_copies(ctx, 0);
+      if (st != MOE_OK) return st;
+    } else if (ctx->p2p) {
       launch_signal(a, b, 2, s);
       LAUNCHED(ctx, 1);
     }
@@ -1205,14 +1450,17 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   // the tiles of this rank's own rows go first (overlapping the peers' NVLink pushes)
   const unsigned* arrived = (ctx->last_gather || ctx->last_direct) ? ctx->sig->flag_exp : ctx->sig->flag_data;
   // (direct dispatch: this rank's own rows are combined by k_expand_direct too -- wait for all)
-  const SrcWait wait1{ctx->p2p ? arrived : nullptr, ctx->seg_src, ctx->G, ctx->last_direct ? -1 : ctx->me,
-                      ctx->epoch_dev, ctx->flag_timeout_ns};
-  const SrcWait nowait{nullptr, nullptr, 0, 0, nullptr, 0};
+  // copy-engine dispatch: per (source, segment) flags, raised after each run's copy,
+  // so K5's phase-B tiles of the first segments start while the later runs still cross
+  const SrcWait wait1{ctx->p2p ? arrived : nullptr, ctx->last_ce ? ctx->sig->flag_se : nullptr, ctx->seg_e, ctx->E,
+                      ctx->seg_src, ctx->G, ctx->last_direct ? -1 : ctx->me, ctx->epoch_dev, ctx->flag_timeout_ns};
+  const SrcWait nowait{nullptr, nullptr, nullptr, 0, nullptr, 0, 0, nullptr, 0};
   const FusedRet plain{nullptr, nullptr, 0, 0};
   // fused combine (P2P): K6's epilogue stores every output row over NVLink into its
   // source rank's return buffer at the item's send-order slot -- the combine
   // all-to-all overlaps the expert GEMM tile by tile
-  const FusedRet fused{ctx->ret_table, ctx->seg_src, ctx->G, ctx->ffn_fused ? 1 : 0};
+  const FusedRet fused{ctx->ret_table, ctx->seg_src, ctx->G, ctx->ffn_fused ? 1 : 0,
+                      (ctx->last_ce && !ctx->ffn_fused) ? ctx->segdone : nullptr};
   // Split-K of the down projection in decode-sized contexts (about one 128-row M tile
   // per hosted expert): when K6's output tiles cannot cover the SMs, split K into S
   // slices (fp32 partials in a workspace, ordered reduction -- deterministic).
@@ -1250,10 +1498,21 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
                                       ctx->gemm_cg, ctx->num_sms, wait1, ctx->err_dev, ctx->done_counter + 2, plain,
                                       s, 1, nullptr, 0, ctx->tmDh);
   if (e != cudaSuccess) return fail(ctx, MOE_ERR_CUDA, "gemm1 launch: %s", cudaGetErrorString(e));
+  if (ctx->last_ce && !ctx->ce_dispatched) {  // single-process group: the dispatch copies now
+    moe_status st = ce_dispatch_copies(ctx);
+    if (st != MOE_OK) return st;
+  }
+  // copy-engine dispatch: the rows return through the copy engines, or -- fused
+  // combine (F/tp <= 8192) -- K6's epilogue stores them as in the SM path
+  const bool ce_return = ctx->last_ce && !ctx->ffn_fused;
   if (rec) CU(cudaEventRecord(ev[1], s));
   tl_rec(ctx, 5, s);
   if (!vslices) {
     const long long pstride = (long long)ctx->cap_rows * H;
+    if (ce_return) {  // K6's per-segment counters start from zero (the copy stream waits on them)
+      CU(cudaMemsetAsync(ctx->segdone, 0, sizeof(unsigned) * ctx->E, s));
+      CU(cudaEventRecord(ctx->ev_k6, s));
+    }
     e = launch_grouped_gemm(ctx->tmA2, ctx->tmB2, ctx->ybuf, H, ctx->seg_meta, ctx->E, n_w, H, F, false,
                             ctx->gemm_cg, ctx->num_sms, nowait, ctx->err_dev, ctx->done_counter + 2, fused, s, ksplit,
                             ctx->splitk_ws, pstride, ctx->tmDy);
@@ -1281,7 +1540,10 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
   }
   tl_rec(ctx, 6, s);
   ctx->launches += 2;
-  if (ctx->p2p) {  // expert outputs of this rank are ready for the peers' combine
+  if (ce_return) {  // the copy engines return the rows and raise flag_y
+    moe_status st = ce_combine_copies(ctx, 1);
+    if (st != MOE_OK) return st;
+  } else if (ctx->p2p) {  // expert outputs of this rank are ready for the peers' combine
     launch_signal(a, b, 2, s);
     LAUNCHED(ctx, 1);
   }
@@ -1297,6 +1559,7 @@ moe_status moe_expert_ffn(moe_ctx_t ctx, const moe_bf16* w13, const moe_bf16* w2
 }
 
 moe_status moe_ffn_timing_enable(moe_ctx_t ctx, int32_t max_records) {
+  DeviceGuard device_guard;
   if (!ctx || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   CU(cudaSetDevice(ctx->cfg.device));
   CU(cudaDeviceSynchronize());
@@ -1321,6 +1584,7 @@ moe_status moe_ffn_timing_read(moe_ctx_t ctx, float* ms, int32_t max_records, in
 }
 
 moe_status moe_timeline_enable(moe_ctx_t ctx, int32_t max_records) {
+  DeviceGuard device_guard;
   if (!ctx || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   CU(cudaSetDevice(ctx->cfg.device));
   CU(cudaDeviceSynchronize());
@@ -1334,6 +1598,7 @@ moe_status moe_timeline_enable(moe_ctx_t ctx, int32_t max_records) {
 }
 
 moe_status moe_timeline_read(moe_ctx_t ctx, float* ms, int32_t max_records, int32_t* n_out) {
+  DeviceGuard device_guard;
   if (!ctx || !ms || !n_out || max_records < 0) return fail(ctx, MOE_ERR_INVALID_ARG, "bad arguments");
   CU(cudaSetDevice(ctx->cfg.device));
   CU(cudaDeviceSynchronize());
@@ -1352,6 +1617,8 @@ moe_status moe_timeline_read(moe_ctx_t ctx, float* ms, int32_t max_records, int3
 
 moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   cudaStream_t s = (cudaStream_t)stream;
   ctx->last_stream = s;
   ctx->ffn_fused = false;  // identity rows stay in the expert-output buffer; combine pulls them
@@ -1369,6 +1636,7 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
   if (ctx->tpi == 0) CU(cudaMemcpyAsync(ctx->ybuf, ctx->recv, ybytes, cudaMemcpyDeviceToDevice, s));
   else CU(cudaMemsetAsync(ctx->ybuf, 0, ybytes, s));  // TP slices > 0 return zeros
   if (ctx->virt && ctx->tp > 1) CU(cudaMemsetAsync(ctx->ybuf + ybytes / 2, 0, ybytes * (ctx->tp - 1), s));
+  if (ctx->last_ce) return ce_combine_copies(ctx, 2);
   if (ctx->p2p) {
     launch_signal(a, b, 2, s);
     LAUNCHED(ctx, 1);
@@ -1378,6 +1646,8 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream) {
 
 moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_t stream) {
   if (!ctx) return fail(ctx, MOE_ERR_INVALID_ARG, "ctx is NULL");
+  DeviceGuard device_guard;
+  CU(cudaSetDevice(ctx->cfg.device));
   if (!ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "moe_combine before moe_dispatch");
   if (ctx->last_T > 0 && (!w || !out)) return fail(ctx, MOE_ERR_INVALID_ARG, "NULL tensor");
   if (ctx->out_stay) return fail(ctx, MOE_ERR_INVALID_ARG, "MOE_OUT_STAY: the outputs go to moe_dispatch_from");
@@ -1438,6 +1708,7 @@ moe_status moe_combine(moe_ctx_t ctx, const float* w, moe_bf16* out, moe_stream_
 // Decode the device plan into the oracle's C3 terms (unpadded receive position
 // on the destination rank, source send-order slot).
 moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, int32_t* send_slot, int32_t* cnt_out) {
+  DeviceGuard device_guard;
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   CU(cudaSetDevice(ctx->cfg.device));
   CU(cudaStreamSynchronize(ctx->last_stream));
@@ -1553,14 +1824,19 @@ moe_status moe_debug_plan(moe_ctx_t ctx, int32_t* dest_rank, int32_t* recv_pos, 
 }
 
 moe_status moe_debug_send(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out) {
+  DeviceGuard device_guard;
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
-  if (!(ctx->comm && !ctx->p2p)) return fail(ctx, MOE_ERR_UNSUPPORTED, "the compact send buffer exists in MOE_A2A_NCCL mode only");
+  const bool ce = ctx->p2p && ctx->last_ce;
+  if (!(ctx->comm && !ctx->p2p) && !ce)
+    return fail(ctx, MOE_ERR_UNSUPPORTED, "a send buffer exists in MOE_A2A_NCCL and copy-engine modes only");
+  if (ce && ctx->local_group && ctx->cnt_host.size() != (size_t)ctx->G * ctx->E)
+    return fail(ctx, MOE_ERR_INVALID_ARG, "single-process group: call after the rank's moe_expert_ffn");
   CU(cudaSetDevice(ctx->cfg.device));
   CU(cudaStreamSynchronize(ctx->last_stream));
   const int E = ctx->E, H = ctx->H;
   int64_t n = 0;
   for (int e = 0; e < E; ++e)
-    if (ctx->P_host[e] != ctx->grp) n += ctx->cnt_host[(size_t)ctx->me * E + e];
+    if (ce || ctx->P_host[e] != ctx->grp) n += ctx->cnt_host[(size_t)ctx->me * E + e];
   if (rows_out) *rows_out = n;
   if (!rows_host) return MOE_OK;
   if (n > max_rows) return fail(ctx, MOE_ERR_CAPACITY, "max_rows too small (%lld)", (long long)n);
@@ -1569,6 +1845,7 @@ moe_status moe_debug_send(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, 
 }
 
 moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out) {
+  DeviceGuard device_guard;
   if (!ctx || !ctx->have_plan) return fail(ctx, MOE_ERR_INVALID_ARG, "no plan");
   CU(cudaSetDevice(ctx->cfg.device));
   if (ctx->p2p) {  // the peers' rows of the last dispatch have landed here

@@ -395,7 +395,8 @@ class MoeLayer:
         return buf[:n.value]
 
     def debug_send(self):
-        """NCCL mode: this rank's compact send buffer (remote rows in C3 send order)."""
+        """NCCL mode: this rank's compact send buffer (remote rows in C3 send order);
+        copy-engine mode: the staging buffer indexed by the C3 send slot (moe.h)."""
         n = ctypes.c_int64()
         self._c(_lib.moe_debug_send(self._ctx, None, 0, ctypes.byref(n)))
         buf = np.zeros((max(n.value, 1), self.H), np.uint16)

@@ -77,6 +77,15 @@ def main():
                             if P[mine[t, j]] != rank))
             ref_send = xb[[a + t for _, t in items]].reshape(-1, H)
             assert np.array_equal(lay.debug_send(), ref_send), "send buffer order"
+        elif os.environ.get("MOE_A2A_CE") == "1":
+            # copy-engine plane: the staging buffer holds every remote row at its C3 slot
+            sl = pl["slot"][rank]
+            mine = ridx[a:b]
+            send = lay.debug_send()
+            for t in range(b - a):
+                for j in range(k):
+                    if P[mine[t, j]] != rank:
+                        assert np.array_equal(send[int(sl[t, j])], xb[a + t]), "staged send row"
         rows = lay.debug_recv()
         ref_rows = xb[[blocks[s][0] + t for (s, t, j, e) in pl["recv"][rank]]].reshape(-1, H)
         assert np.array_equal(rows, ref_rows), "received payload"

@@ -586,7 +586,8 @@ def test_group_random_configs_match_virtual(cuda_ok, seed, G, tp, T, H, F, E, k)
 
 
 @pytest.mark.multigpu
-@pytest.mark.parametrize("E,k,tp,fused", [(64, 8, 1, "1"), (8, 2, 2, "0"), (8, 2, 2, "1"), (16, 4, 1, "0")])
+@pytest.mark.parametrize("E,k,tp,fused", [(64, 8, 1, "1"), (8, 2, 2, "0"), (8, 2, 2, "1"), (16, 4, 1, "0"),
+                                          (64, 8, 1, "ce"), (16, 4, 1, "ce")])
 def test_group_eight_ranks_over_devices(cuda_ok, E, k, tp, fused, monkeypatch):
     """An 8-rank group over the box's GPUs (2 ranks per GPU on 4 GPUs, 4 on 2):
     8EP at E64 top-8 (D5's shape scaled down) and 4EP-2TP (the 8-GPU TP config),
@@ -597,7 +598,11 @@ def test_group_eight_ranks_over_devices(cuda_ok, E, k, tp, fused, monkeypatch):
     if nd < 2:
         pytest.skip("needs >= 2 GPUs")
     nd = 4 if nd >= 4 else 2
-    monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
+    if fused == "ce":                        # copy-engine data plane (256-row GEMM tiles)
+        monkeypatch.setenv("MOE_A2A_CE", "1")
+        monkeypatch.setenv("MOE_GEMM_CG", "2")
+    else:
+        monkeypatch.setenv("MOE_FUSED_COMBINE", fused)
     moe = _moe()
     G, T, H, F = 8, 3001, 256, 512
     n_grp = G // tp
@@ -652,3 +657,66 @@ def test_group_eight_ranks_over_devices(cuda_ok, E, k, tp, fused, monkeypatch):
         torch.cuda.synchronize(d)
     for lay in lays:
         lay.close()
+
+
+@pytest.mark.parametrize("seed,G,tp,T,H,F,E,k", [c for c in RANDOM_CONFIGS if c[2] == 1])
+def test_group_copy_engine_data_plane(cuda_ok, seed, G, tp, T, H, F, E, k, monkeypatch):
+    """MOE_A2A_CE=1: the peers' rows staged in send order and moved by the copy
+    engines (one peer copy per (destination, expert) run, flags by stream memory
+    writes), the expert outputs returned per segment as K6 finishes it (stream waits
+    on K6's segment counters): bit-exact with the virtual-rank run, the identity
+    round trip bit-exact, the received payload in the oracle's order."""
+    monkeypatch.setenv("MOE_A2A_CE", "1")
+    monkeypatch.setenv("MOE_GEMM_CG", "2")        # the copy-engine plane runs with 256-row tiles
+    moe = _moe()
+    rng = np.random.default_rng(seed)
+    P = rng.integers(0, G, E)
+    inp = Inputs(T, H, F, E, k, s=float(rng.uniform(0.0, 1.8)), seed=100 + seed)
+    g = Group(G, T, H, F, E, k)
+    x_all, logits_all, xs, ls = _setup(inp, g, k)
+    ridx, _ = oroute.route(inp.logits.numpy(), k)
+    xb = inp.x.view(torch.int16).numpy().view(np.uint16)
+    w1a, w3a, w2a = inp.device_weights(DEV, list(range(E)))
+    ws = []
+    for r in range(G):
+        hosted = [e for e in range(E) if P[e] == r]
+        if hosted:
+            sel = torch.tensor(hosted, device=DEV)
+            ws.append((moe.pack_w13(w1a[sel], w3a[sel]), w2a[sel].contiguous()))
+        else:
+            ws.append((None, None))
+    for lay in g.lays:
+        lay.placement(P)
+    torch.cuda.synchronize()
+    pl = oplan.plan([ridx[a:b] for a, b in g.blocks], P, G)
+    # identity round trip; the payload is read after the identity FFN (a single-process
+    # group queues a rank's dispatch copies in its FFN call, see moe.h)
+    rw = g.each(lambda r, lay: lay.route(ls[r], k))
+    g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+    g.each(lambda r, lay: lay.identity_ffn())
+    for r, lay in enumerate(g.lays):
+        rows = lay.debug_recv()
+        ref_rows = xb[[g.blocks[s][0] + t for (s, t, j, e) in pl["recv"][r]]].reshape(-1, H)
+        assert np.array_equal(rows, ref_rows), f"received payload of rank {r}"
+        # the staging buffer the copy engines read: a peer's row at its C3 send slot
+        a, b = g.blocks[r]
+        send = lay.debug_send()
+        sl = pl["slot"][r]
+        mine = ridx[a:b]
+        remote = [(int(sl[t, j]), t) for t in range(b - a) for j in range(k) if P[mine[t, j]] != r]
+        for slot, t in remote:
+            assert np.array_equal(send[slot], xb[a + t]), f"staged row (rank {r}, slot {slot})"
+    outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+    g.sync()
+    for r in range(G):
+        assert torch.equal(outs[r].view(torch.int16), xs[r].view(torch.int16)), "identity round trip"
+    virt = _virtual_out(inp, P, G, k)
+    for rep in range(2):                     # the second layer reuses every buffer
+        rw = g.each(lambda r, lay: lay.route(ls[r], k))
+        g.each(lambda r, lay: lay.dispatch(xs[r], rw[r][0], P))
+        g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
+        outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
+        g.sync()
+        out = torch.cat(outs)
+        assert torch.equal(out.view(torch.int16), virt.view(torch.int16)), f"copy-engine plane vs virtual ({rep})"
+    g.close()

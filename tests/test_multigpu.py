@@ -19,18 +19,21 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("a2a", ["nccl", "p2p", "p2p_fused", "p2p_gather"])
+@pytest.mark.parametrize("a2a", ["nccl", "p2p", "p2p_fused", "p2p_gather", "p2p_ce"])
 @pytest.mark.parametrize("n", [2, 4])
 def test_ep_over_real_ranks(n, a2a):
     if _ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
-    port = 29600 + n + {"nccl": 0, "p2p": 7, "p2p_fused": 13, "p2p_gather": 19}[a2a] + os.getpid() % 500
+    port = 29600 + n + {"nccl": 0, "p2p": 7, "p2p_fused": 13, "p2p_gather": 19, "p2p_ce": 25}[a2a] + os.getpid() % 500
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MOE_TEST_A2A=a2a.split("_")[0])
     if a2a == "p2p_fused":
         env["MOE_FUSED_COMBINE"] = "1"       # K6 epilogue returns rows over NVLink
     env["MOE_DISPATCH"] = "gather" if a2a == "p2p_gather" else "scatter"
+    if a2a == "p2p_ce":                      # copy-engine data plane (256-row GEMM tiles)
+        env["MOE_A2A_CE"] = "1"
+        env["MOE_GEMM_CG"] = "2"
     # own process group, so a hung rank is killed together with the launcher
     p = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True, cwd=ROOT, env=env,
                          start_new_session=True)
