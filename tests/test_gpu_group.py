@@ -472,14 +472,19 @@ def synth_logits(T, E, seed):
     return synth.zipf_logits(T, E, 1.6, seed=seed).to(DEV)
 
 
-@pytest.mark.parametrize("P,s", [([0, 1, 2, 2, 3, 2, 3, 3], 1.6), ([0, 0, 1, 1, 2, 2, 3, 3], 0.0)])
-def test_group_mixtral_full_size_every_tile(cuda_ok, P, s):
+@pytest.mark.parametrize("P,s,ce", [([0, 1, 2, 2, 3, 2, 3, 3], 1.6, False), ([0, 0, 1, 1, 2, 2, 3, 3], 0.0, False),
+                                    ([0, 1, 2, 2, 3, 2, 3, 3], 1.6, True)])
+def test_group_mixtral_full_size_every_tile(cuda_ok, P, s, ce, monkeypatch):
     """The bench's 4EP configuration at full size -- Mixtral layer (E8 top-2, H4096,
     F14336), T = 16384 tokens over 4 real P2P ranks on one GPU, ILP-1 balanced
     placement at s = 1.6 (D3) and contiguous at s = 0 (D2) -- checked against the
     oracle on tokens covering every 256-row M tile of every expert segment (on
     each hosting rank, an expert's rows are ordered by source, then token: the
-    global token order, as in the virtual-rank layout)."""
+    global token order, as in the virtual-rank layout).  ce: the copy-engine data
+    plane (MOE_A2A_CE=1; F = 14336 > 8192, so the rows return by copy engine per
+    K6 segment)."""
+    if ce:
+        monkeypatch.setenv("MOE_A2A_CE", "1")
     import synth
     from tests.test_gpu_parity import tile_cover_tokens
     moe = _moe()
@@ -504,6 +509,8 @@ def test_group_mixtral_full_size_every_tile(cuda_ok, P, s):
     g.each(lambda r, lay: lay.expert_ffn(*ws[r]))
     outs = g.each(lambda r, lay: lay.combine(rw[r][1]))
     g.sync()
+    if ce:   # the staging buffer exists only when the copy-engine plane ran
+        assert g.lays[0].debug_send().shape[0] == rw[0][0].numel()   # rank 0's routed items
     out = torch.cat(outs)
     gidx = torch.cat([q[0] for q in rw]).cpu().numpy()
     sel = tile_cover_tokens(gidx, E, 256, seed=7)
