@@ -320,7 +320,10 @@ moe_status moe_debug_identity_ffn(moe_ctx_t ctx, moe_stream_t stream);
 moe_status moe_debug_send(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out);
 
 /* Copies the received rows of the last dispatch, in unpadded receive order of
- * this process (virtual: rank 0's rows first, ...), to host bf16 [rows][H]. */
+ * this process (virtual: rank 0's rows first, ...), to host bf16 [rows][H].
+ * P2P: waits for every source's rows first (a latched flag timeout is returned);
+ * copy-engine mode in a single-process group: after every rank's moe_expert_ffn
+ * (which queues that rank's copies). */
 moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, int64_t* rows_out);
 
 /* Number of kernels this context has launched since creation (for the bench's

@@ -1854,6 +1854,10 @@ moe_status moe_debug_recv(moe_ctx_t ctx, moe_bf16* rows_host, int64_t max_rows, 
                 ctx->epoch_dev, ctx->err_dev, ctx->flag_timeout_ns, ctx->last_stream);
   }
   CU(cudaStreamSynchronize(ctx->last_stream));
+  {  // a flag wait that timed out (e.g. the rows were never sent) surfaces here
+    moe_status st = check_device_error(ctx);
+    if (st != MOE_OK) return st;
+  }
   const int E = ctx->E, H = ctx->H;
   std::vector<int32_t> meta(1 + 3 * E + 4);
   CU(cudaMemcpy(meta.data(), ctx->seg_meta, sizeof(int32_t) * meta.size(), cudaMemcpyDeviceToHost));
