@@ -145,7 +145,7 @@ struct moe_ctx {
   bool last_ce = false;
   cudaEvent_t ev_cnt = nullptr, ev_staged = nullptr, ev_k6 = nullptr, ev_side2 = nullptr;
   cudaStream_t side2 = nullptr;         // second copy-engine stream (the combine's runs alternate)
-  int32_t* ce_pinned = nullptr;         // host: count matrix [G][E], placement [E], epoch
+  int32_t* ce_pinned = nullptr;         // host: count matrix [G][E], placement [E], epoch, error word
   unsigned* segdone = nullptr;          // [E] K6 per-segment completion counters
   std::vector<void*> recv_h, sig_h, ret_h;  // host copies of the peer tables (P2P)
   bool ce_dispatched = false;           // this dispatch's copies are queued
@@ -522,7 +522,7 @@ static moe_status ctx_alloc(const moe_config& c, int share, moe_ctx_t* out) {
   cudaMemset(ctx->seg_meta, 0, sizeof(int32_t) * (1 + 3 * E + 4));
   if (cudaMallocHost((void**)&ctx->P_all_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->cnt_pinned, sizeof(int32_t) * (size_t)G * E) != cudaSuccess ||
-      cudaMallocHost((void**)&ctx->ce_pinned, sizeof(int32_t) * ((size_t)G * E + E + 1)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->ce_pinned, sizeof(int32_t) * ((size_t)G * E + E + 2)) != cudaSuccess ||
       cudaMalloc((void**)&ctx->segdone, sizeof(unsigned) * (size_t)E) != cudaSuccess)
     return fail(ctx, MOE_ERR_CUDA, "cudaMallocHost failed");
   ctx->P_host.assign(E, 0);
@@ -1067,6 +1067,7 @@ static moe_status dispatch_impl(moe_ctx_t ctx, const moe_bf16* x, const int32_t*
     CU(cudaMemcpyAsync(ctx->ce_pinned + (size_t)G * E, ctx->P_dev, sizeof(int32_t) * E, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(ctx->ce_pinned + (size_t)G * E + E, ctx->epoch_dev, sizeof(unsigned), cudaMemcpyDeviceToHost,
                        s));
+    CU(cudaMemcpyAsync(ctx->ce_pinned + (size_t)G * E + E + 1, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost, s));
     CU(cudaEventRecord(ctx->ev_cnt, s));
   }
   if (direct && !ctx->p2p) {
@@ -1281,6 +1282,10 @@ static moe_status ce_dispatch_copies(moe_ctx_t ctx) {
   const int32_t* cnt = ctx->ce_pinned;
   const int32_t* P = cnt + (size_t)G * E;
   ctx->ce_epoch = (unsigned)cnt[(size_t)G * E + E];
+  // a failed count exchange (timeout, placement mismatch, capacity) leaves the counts
+  // unusable: queue no copy (the error word stays latched for moe_ctx_sync)
+  if (cnt[(size_t)G * E + E + 1] != 0)
+    return fail(ctx, MOE_ERR_DEVICE, "device error latched before the copy-engine dispatch (see moe_ctx_sync)");
   for (int e = 0; e < E; ++e)
     if (P[e] < 0 || P[e] >= G) return fail(ctx, MOE_ERR_DEVICE, "expert_to_rank[%d]=%d outside [0, %d)", e, P[e], G);
   ctx->cnt_host.assign(cnt, cnt + (size_t)G * E);
@@ -1306,6 +1311,9 @@ static moe_status ce_dispatch_copies(moe_ctx_t ctx) {
       if (j >= runs[g].size()) continue;
       const int e = runs[g][j];
       const int n = cnt[me * E + e];
+      if ((int64_t)ctx->ce_recv_base[me * E + e] + n > ctx->cap_rows ||
+          (int64_t)ctx->ce_send_base[me * E + e] + n > ctx->send_rows)
+        return fail(ctx, MOE_ERR_CAPACITY, "copy-engine dispatch run outside the buffers");
       CU(cudaMemcpyAsync(static_cast<char*>(ctx->recv_h[g]) + (size_t)ctx->ce_recv_base[me * E + e] * rowb,
                          reinterpret_cast<char*>(ctx->sendbuf) + (size_t)ctx->ce_send_base[me * E + e] * rowb,
                          n * rowb, cudaMemcpyDeviceToDevice, cs));
