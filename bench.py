@@ -4,7 +4,7 @@ contiguous placement (BASELINE.json metric), through libmoe's C ABI.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config mixtral|tiny|e64] [--zipf-s S] [--placement contiguous|balanced|both]
-                    [--tp T] [--a2a p2p|nccl]
+                    [--tp T] [--a2a p2p|nccl|ce]
 
 A step is one pass of the whole hot path over one
 batch: moe_route -> moe_route_stats (layer l-1 -> l) -> moe_dispatch ->
@@ -15,7 +15,8 @@ synthetic bf16 data, random-init weights.  T is split across the N EP ranks
 (strong scaling); N = 1 hosts all 8 experts on one GPU.  ``--tp t`` runs tensor
 parallelism inside the experts (N/t EP groups of t ranks, reading G20); the
 default is t = 2 for the Mixtral layer on 8 GPUs (BASELINE configs[3], the
-paper's 4EP-2TP) and t = 1 otherwise.
+paper's 4EP-2TP) and t = 1 otherwise.  ``--a2a ce`` runs the all-to-all on the
+copy engines (MOE_A2A_CE=1; the default is the SM/TMA P2P path).
 
 Timing: W untimed warm-up steps, then K steps bracketed by a barrier and a
 device synchronize on both sides, CUDA events on the launching stream, max over
@@ -251,7 +252,7 @@ def run_ours(args):
     grp, tpq = rank // tp, rank % tp
     Fl = F // tp                # FFN columns this rank computes (TP slice, reading G20)
     lay = moe.MoeLayer(max_tokens=max(Tmax, 1), hidden=H, ffn=F, num_experts=E, max_k=k, world=N, rank=rank,
-                       device=local, uid=uid, a2a=args.a2a, tp=tp)
+                       device=local, uid=uid, a2a="p2p" if args.a2a == "ce" else args.a2a, tp=tp)
     s = args.zipf_s
     x = synth.hidden_states(T, H, args.seed, device=dev)[t0:t1].contiguous()
     logits = synth.zipf_logits(T, E, s, args.seed, device=dev)[t0:t1].contiguous()
@@ -621,7 +622,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded Zipf logits, N(0,1) tokens, random-init weights)",
             "config": {"workload": cfg["workload"], "experts": E, "top_k": k, "hidden": H, "ffn": F,
                        "tokens_total": T, "ep": G, "tp": tp, "placement": head, "zipf_s": s, "seed": args.seed,
-                       "a2a": args.a2a if N > 1 else "none (single GPU)",
+                       "a2a": (args.a2a if args.a2a != "ce" else "p2p + copy-engine data plane (MOE_A2A_CE=1)")
+                       if N > 1 else "none (single GPU)",
                        "l2": "no flush: inputs larger than L2 (expert weights 2.8 GB, activations 128 MiB)"
                        if args.config == "mixtral" else "no flush"},
             "p50_ms": r["p50_ms"], "p99_ms": r["p99_ms"], "mean_over_ranks_ms": r["mean_over_ranks_ms"],
@@ -713,8 +715,9 @@ def main():
     ap.add_argument("--zipf-s", type=float, default=1.6)
     ap.add_argument("--placement", choices=["contiguous", "balanced", "both"], default="both")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--a2a", choices=["nccl", "p2p"], default="p2p",
-                    help="all-to-all transport between real ranks (N > 1)")
+    ap.add_argument("--a2a", choices=["nccl", "p2p", "ce"], default="p2p",
+                    help="all-to-all transport between real ranks (N > 1); ce = P2P with the copy-engine "
+                         "data plane (MOE_A2A_CE=1)")
     ap.add_argument("--tp", type=int, default=None,
                     help="tensor-parallel ranks per expert (EP groups = gpus / tp; reading G20); default 2 for "
                          "the Mixtral layer on 8 GPUs (BASELINE configs[3]: 4EP-2TP on 8 B200), else 1")
@@ -723,6 +726,8 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=32)
     args = ap.parse_args()
+    if args.a2a == "ce":
+        os.environ["MOE_A2A_CE"] = "1"   # read by libmoe at each dispatch
     if args.tp is None:
         args.tp = 2 if (args.gpus == 8 and args.config == "mixtral") else 1
     if args.warmup < 3 and args.impl == "ours":
