@@ -851,9 +851,9 @@ moe_status moe_ctx_destroy(moe_ctx_t ctx) {
   return MOE_OK;
 }
 
-static moe_status check_device_error(moe_ctx_t ctx) {
-  int e = 0;
-  CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+// Report a latched device error word e (and clear the word): the message names every
+// set bit and every timed-out wait site.
+static moe_status report_device_error(moe_ctx_t ctx, int e) {
   if (e) {
     cudaMemset(ctx->err_dev, 0, sizeof(int));
     std::string sites;
@@ -873,6 +873,12 @@ static moe_status check_device_error(moe_ctx_t ctx) {
                 sites.c_str());
   }
   return MOE_OK;
+}
+
+static moe_status check_device_error(moe_ctx_t ctx) {
+  int e = 0;
+  CU(cudaMemcpy(&e, ctx->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  return report_device_error(ctx, e);
 }
 
 moe_status moe_ctx_sync(moe_ctx_t ctx) {
@@ -1284,8 +1290,7 @@ static moe_status ce_dispatch_copies(moe_ctx_t ctx) {
   ctx->ce_epoch = (unsigned)cnt[(size_t)G * E + E];
   // a failed count exchange (timeout, placement mismatch, capacity) leaves the counts
   // unusable: queue no copy (the error word stays latched for moe_ctx_sync)
-  if (cnt[(size_t)G * E + E + 1] != 0)
-    return fail(ctx, MOE_ERR_DEVICE, "device error latched before the copy-engine dispatch (see moe_ctx_sync)");
+  if (cnt[(size_t)G * E + E + 1] != 0) return report_device_error(ctx, cnt[(size_t)G * E + E + 1]);
   for (int e = 0; e < E; ++e)
     if (P[e] < 0 || P[e] >= G) return fail(ctx, MOE_ERR_DEVICE, "expert_to_rank[%d]=%d outside [0, %d)", e, P[e], G);
   ctx->cnt_host.assign(cnt, cnt + (size_t)G * E);
